@@ -1,0 +1,95 @@
+/*
+ * im2win_sm100.h — C ABI of libim2win_sm100.so, the B200 (sm_100a) im2win
+ * transform and im2win convolution.
+ *
+ * The reference (`winconv`, pure Python + numba) has no C ABI: its native
+ * seam is two numba kernels that already follow the "caller allocates, flat
+ * buffers + integer scalars, no return value" convention.  Each entry point
+ * below replaces one of them one-for-one:
+ *
+ *   im2win_transform_f32   <- _im2win_fill(src, dst, h_f, w_eff, stride)
+ *                             /root/reference/pkg/src/winconv/layouts.py:73-83,
+ *                             called from im2win() at layouts.py:94
+ *   im2win_conv_f32        <- _tiled_kernel(windows_flat, flt_flat, out_flat,
+ *                             dim_m, dim_n, dim_k, c_in, c_out, h_out, w_out,
+ *                             row_len, h_f, w_f, stride, m_b, n_b, k_b, m_t,
+ *                             n_t, use_vec, use_pf)
+ *                             kernels/optimized.py:66-214, called from
+ *                             compute_from_windows_opt() at optimized.py:228-233
+ *
+ * Conventions (same as the reference seam):
+ *   - every pointer is device memory on the current CUDA device; the caller
+ *     allocates all outputs and the optional workspace (layouts.py:93,
+ *     optimized.py:226); the library never allocates device memory;
+ *   - tensors are float32, C-contiguous, NCHW (tensors.py:1-6);
+ *   - validation of shapes/geometry happens in the host layer before the
+ *     call (ShapeError / GeometryError / PlanError, errors.py:4-33); the
+ *     library re-checks index ranges and returns nonzero on violation;
+ *   - work is enqueued on `stream` (a cudaStream_t; NULL = legacy default
+ *     stream) and the call returns without synchronising;
+ *   - return 0 on success; nonzero = error, message via im2win_last_error().
+ */
+#ifndef IM2WIN_SM100_H
+#define IM2WIN_SM100_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Arithmetic variants of the convolution. */
+enum im2win_variant {
+  IM2WIN_FP32_EXACT = 0, /* FMUL+FADD, ascending k: bit-exact with the reference */
+  IM2WIN_FP32_FMA = 1,   /* FFMA, ascending k: within 1e-4 of the reference        */
+  IM2WIN_TF32 = 2,       /* tcgen05 kind::tf32, fp32 accumulate in TMEM            */
+  IM2WIN_BF16 = 3        /* tcgen05 kind::f16 (bf16 operands), fp32 accumulate     */
+};
+
+/* GPU tile plan; mirrors winconv TilePlan (kernels/plan.py:11-48).
+ * block_cfg < 0 lets the library pick the tile for the shape. */
+typedef struct im2win_tile_plan {
+  int32_t block_cfg;              /* index of a compiled CTA tile, or -1        */
+  int32_t micro_kernel;           /* 1: 8x8 register micro-tile; 0: 1x1         */
+  int32_t vectorized_load;        /* 1: 128-bit shared-memory fragment loads     */
+  int32_t prefetch_double_buffer; /* 1: multi-stage async prefetch ring          */
+} im2win_tile_plan;
+
+/* Window-order transform (layouts.py:73-95).
+ * src: (n, c, h, w) float32; dst: (n, c, h_out, h_f * w_eff) float32 where
+ * h_out = (h - h_f) / stride + 1, w_eff = (w_out - 1) * stride + w_f.
+ * Bit-exact copy: dst[i,r,m,col*h_f+u] = src[i,r,m*stride+u,col]. */
+int im2win_transform_f32(const float* src, float* dst, int64_t n, int64_t c, int64_t h,
+                         int64_t w, int32_t h_f, int32_t w_f, int32_t stride, void* stream);
+
+/* Bytes of device workspace im2win_conv_f32 needs (packed filter + offsets). */
+size_t im2win_conv_workspace_bytes(int64_t c_in, int64_t c_out, int32_t h_f, int32_t w_f,
+                                   int32_t variant);
+
+/* im2win convolution on an already-transformed input (optimized.py:217-234).
+ * windows: (n, c_in, h_out, row_len) from im2win_transform_f32;
+ * flt: (c_out, c_in, h_f, w_f); out: (n, c_out, h_out, w_out).
+ * plan may be NULL (library default). */
+int im2win_conv_f32(const float* windows, const float* flt, float* out, int64_t n, int64_t c_in,
+                    int64_t c_out, int64_t h_out, int64_t w_out, int64_t row_len, int32_t h_f,
+                    int32_t w_f, int32_t stride, const im2win_tile_plan* plan, int32_t variant,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* Measurement utility (bench.py only): launches `blocks` x 256 threads that each
+ * retire 2*16*iters flops of independent FP32 multiply-add chains; exact != 0
+ * issues FMUL+FADD (the conv's bit-exact pair), else FFMA.  Used to measure the
+ * CUDA-core FP32 roofline denominator on the box (not in MEASURED_PEAKS.json). */
+int im2win_bench_fp32_peak(float* sink, int32_t exact, int32_t iters, int32_t blocks, void* stream);
+
+/* Message of the last failing call on this host thread ("" if none). */
+const char* im2win_last_error(void);
+
+/* ABI version of this library (major*100 + minor). */
+int32_t im2win_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IM2WIN_SM100_H */

@@ -1,0 +1,84 @@
+"""ctypes binding of libim2win_sm100.so (the C ABI in include/im2win_sm100.h).
+
+There is no fallback: if the shared library is missing or cannot be loaded,
+every entry point raises.  Only plain pointers, integers and a stream handle
+cross the boundary.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+from .errors import KernelError
+
+LIB_PATH = Path(__file__).resolve().parent / "libim2win_sm100.so"
+
+# enum im2win_variant
+FP32_EXACT = 0
+FP32_FMA = 1
+TF32 = 2
+BF16 = 3
+VARIANTS = {"fp32-exact": FP32_EXACT, "fp32-fma": FP32_FMA, "tf32": TF32, "bf16": BF16}
+
+# every symbol include/im2win_sm100.h declares
+EXPORTED_SYMBOLS = (
+    "im2win_transform_f32",
+    "im2win_conv_workspace_bytes",
+    "im2win_conv_f32",
+    "im2win_last_error",
+    "im2win_abi_version",
+    "im2win_bench_fp32_peak",
+)
+
+
+class TilePlanC(ctypes.Structure):
+    _fields_ = [
+        ("block_cfg", ctypes.c_int32),
+        ("micro_kernel", ctypes.c_int32),
+        ("vectorized_load", ctypes.c_int32),
+        ("prefetch_double_buffer", ctypes.c_int32),
+    ]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(path: Path | str | None = None) -> ctypes.CDLL:
+    """Load (once) and type the library; raises if it is absent."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path is not None else LIB_PATH
+        if not p.exists():
+            raise ImportError(
+                f"{p} is missing: build it with `python -m paper_2306_14316_b200.build` "
+                "(this package has no CPU fallback)"
+            )
+        lib = ctypes.CDLL(str(p))
+        i64, i32, vp, sz = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t
+        lib.im2win_transform_f32.argtypes = [vp, vp, i64, i64, i64, i64, i32, i32, i32, vp]
+        lib.im2win_transform_f32.restype = ctypes.c_int
+        lib.im2win_conv_workspace_bytes.argtypes = [i64, i64, i32, i32, i32]
+        lib.im2win_conv_workspace_bytes.restype = sz
+        lib.im2win_conv_f32.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i32, i32, i32,
+                                        ctypes.POINTER(TilePlanC), i32, vp, sz, vp]
+        lib.im2win_conv_f32.restype = ctypes.c_int
+        lib.im2win_last_error.argtypes = []
+        lib.im2win_last_error.restype = ctypes.c_char_p
+        lib.im2win_abi_version.argtypes = []
+        lib.im2win_abi_version.restype = ctypes.c_int32
+        lib.im2win_bench_fp32_peak.argtypes = [vp, i32, i32, i32, vp]
+        lib.im2win_bench_fp32_peak.restype = ctypes.c_int
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = load().im2win_last_error().decode(errors="replace")
+        raise KernelError(f"CUDA library error {rc}: {msg}")

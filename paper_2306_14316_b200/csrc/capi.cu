@@ -1,0 +1,125 @@
+// extern "C" boundary of libim2win_sm100.so (declared in include/im2win_sm100.h).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/im2win_sm100.h"
+
+int im2win_launch_transform(const float* src, float* dst, int64_t n, int64_t c, int64_t h, int64_t w,
+                            int h_f, int w_f, int stride, int64_t h_out, int64_t w_eff,
+                            cudaStream_t stream, const char** err);
+int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void* workspace,
+                            int64_t n, int64_t c_in, int64_t c_out, int64_t h_out, int64_t w_out,
+                            int64_t row_len, int h_f, int w_f, int stride, int cfg, int exact,
+                            int vec, int stages, cudaStream_t stream, const char** err);
+int im2win_launch_conv_simt_1x1(const float* win, const float* flt, float* out, void* workspace,
+                                int64_t n, int64_t c_in, int64_t c_out, int64_t h_out,
+                                int64_t w_out, int64_t row_len, int h_f, int w_f, int stride,
+                                int exact, int stages, cudaStream_t stream, const char** err);
+size_t im2win_simt_workspace_bytes(int64_t c_out, int64_t K);
+size_t im2win_tc_workspace_bytes(int64_t c_out, int64_t K, int variant);
+int im2win_launch_conv_tc(const float* win, const float* flt, float* out, void* workspace,
+                          int64_t n, int64_t c_in, int64_t c_out, int64_t h_out, int64_t w_out,
+                          int64_t row_len, int h_f, int w_f, int stride, int variant, int cfg,
+                          cudaStream_t stream, const char** err);
+
+static thread_local char g_last_error[512] = "";
+
+static int fail(int code, const char* msg) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s", msg ? msg : "unknown error");
+  return code;
+}
+
+// The library links its own (static) CUDA runtime, whose current-device state
+// is independent of the caller's.  Every entry point therefore makes the
+// device that owns the output buffer current before launching.
+static int bind_device_of(const void* ptr) {
+  cudaPointerAttributes attr;
+  cudaError_t e = cudaPointerGetAttributes(&attr, ptr);
+  if (e != cudaSuccess) return fail(2, cudaGetErrorString(e));
+  if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged)
+    return fail(1, "pointer is not device memory");
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != attr.device) {
+    e = cudaSetDevice(attr.device);
+    if (e != cudaSuccess) return fail(2, cudaGetErrorString(e));
+  }
+  return 0;
+}
+
+extern "C" {
+
+const char* im2win_last_error(void) { return g_last_error; }
+
+int32_t im2win_abi_version(void) { return 100; }
+
+int im2win_transform_f32(const float* src, float* dst, int64_t n, int64_t c, int64_t h, int64_t w,
+                         int32_t h_f, int32_t w_f, int32_t stride, void* stream) {
+  g_last_error[0] = '\0';
+  if (!src || !dst) return fail(1, "im2win_transform_f32: null pointer");
+  if (n < 1 || c < 1 || h < 1 || w < 1 || h_f < 1 || w_f < 1 || stride < 1)
+    return fail(1, "im2win_transform_f32: extents must be positive");
+  if (h_f > h || w_f > w) return fail(1, "im2win_transform_f32: filter larger than input");
+  if (int rc = bind_device_of(dst)) return rc;
+  const int64_t h_out = (h - h_f) / stride + 1;
+  const int64_t w_out = (w - w_f) / stride + 1;
+  const int64_t w_eff = (w_out - 1) * stride + w_f;
+  const char* err = nullptr;
+  int rc = im2win_launch_transform(src, dst, n, c, h, w, h_f, w_f, stride, h_out, w_eff,
+                                   static_cast<cudaStream_t>(stream), &err);
+  return rc ? fail(rc, err) : 0;
+}
+
+size_t im2win_conv_workspace_bytes(int64_t c_in, int64_t c_out, int32_t h_f, int32_t w_f,
+                                   int32_t variant) {
+  const int64_t K = c_in * h_f * w_f;
+  if (variant == IM2WIN_TF32 || variant == IM2WIN_BF16) return im2win_tc_workspace_bytes(c_out, K, variant);
+  return im2win_simt_workspace_bytes(c_out, K);
+}
+
+int im2win_conv_f32(const float* windows, const float* flt, float* out, int64_t n, int64_t c_in,
+                    int64_t c_out, int64_t h_out, int64_t w_out, int64_t row_len, int32_t h_f,
+                    int32_t w_f, int32_t stride, const im2win_tile_plan* plan, int32_t variant,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_error[0] = '\0';
+  if (!windows || !flt || !out) return fail(1, "im2win_conv_f32: null pointer");
+  if (n < 1 || c_in < 1 || c_out < 1 || h_out < 1 || w_out < 1 || h_f < 1 || w_f < 1 || stride < 1)
+    return fail(1, "im2win_conv_f32: extents must be positive");
+  const int64_t w_eff = (w_out - 1) * stride + w_f;
+  if (row_len != h_f * w_eff) return fail(1, "im2win_conv_f32: row_len != h_f * w_eff");
+  if (workspace_bytes < im2win_conv_workspace_bytes(c_in, c_out, h_f, w_f, variant) || !workspace)
+    return fail(1, "im2win_conv_f32: workspace too small");
+  if (int rc = bind_device_of(out)) return rc;
+  im2win_tile_plan def = {-1, 1, 1, 1};
+  const im2win_tile_plan* p = plan ? plan : &def;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const char* err = nullptr;
+  int rc = 0;
+  switch (variant) {
+    case IM2WIN_FP32_EXACT:
+    case IM2WIN_FP32_FMA: {
+      const int exact = variant == IM2WIN_FP32_EXACT;
+      const int stages = p->prefetch_double_buffer ? 3 : 1;
+      if (!p->micro_kernel)
+        rc = im2win_launch_conv_simt_1x1(windows, flt, out, workspace, n, c_in, c_out, h_out, w_out,
+                                         row_len, h_f, w_f, stride, exact, stages, st, &err);
+      else
+        rc = im2win_launch_conv_simt(windows, flt, out, workspace, n, c_in, c_out, h_out, w_out,
+                                     row_len, h_f, w_f, stride, p->block_cfg, exact,
+                                     p->vectorized_load, stages, st, &err);
+      break;
+    }
+    case IM2WIN_TF32:
+    case IM2WIN_BF16:
+      rc = im2win_launch_conv_tc(windows, flt, out, workspace, n, c_in, c_out, h_out, w_out, row_len,
+                                 h_f, w_f, stride, variant, p->block_cfg, st, &err);
+      break;
+    default:
+      return fail(1, "im2win_conv_f32: unknown variant");
+  }
+  return rc ? fail(rc, err) : 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+"""im2win convolution entry points (drop-in for winconv.kernels.optimized).
+
+`compute_from_windows_opt` mirrors /root/reference/pkg/src/winconv/kernels/optimized.py:217-234
+and `conv_im2win_opt` mirrors :237-241.  The tiled kernel (`_tiled_kernel`,
+:66-214) is the sm_100a library behind `im2win_conv_f32`.
+
+Extra keyword `variant` (default "fp32-exact") selects the arithmetic:
+  fp32-exact  FMUL+FADD, ascending k  -> bitwise equal to the reference
+  fp32-fma    FFMA, ascending k       -> within 1e-4 (max_rel_diff)
+  tf32, bf16  tcgen05 tensor cores    -> within the stated normalized tolerance
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .errors import ShapeError
+from .layouts import Im2winTensor, im2win
+from .plan import GemmDims, TilePlan, to_c_plan
+from .tensors import DTYPE, ConvParams, Tensor4, check_conv_operands
+
+_workspaces: dict[tuple, torch.Tensor] = {}
+
+
+def _workspace(device: torch.device, stream: int, nbytes: int) -> torch.Tensor:
+    key = (device.index, stream)
+    buf = _workspaces.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+        _workspaces[key] = buf
+    return buf
+
+
+def _variant_code(variant: str) -> int:
+    try:
+        return _lib.VARIANTS[variant]
+    except KeyError:
+        raise ValueError(f"unknown variant {variant!r}, expected one of {tuple(_lib.VARIANTS)}") from None
+
+
+def conv_windows_into(win: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, params: ConvParams,
+                      w_eff: int, plan: TilePlan | None = None, variant: str = "fp32-exact") -> None:
+    """Launch the convolution into a caller-allocated output (the optimized.py:228-233 seam)."""
+    n_img, c_in, h_out, row_len = (int(d) for d in win.shape)
+    w_out = int(out.shape[3])
+    code = _variant_code(variant)
+    lib = _lib.load()
+    nbytes = lib.im2win_conv_workspace_bytes(c_in, params.c_out, params.h_f, params.w_f, code)
+    stream = torch.cuda.current_stream(win.device).cuda_stream
+    ws = _workspace(win.device, stream, nbytes)
+    cplan = to_c_plan(plan)
+    with torch.cuda.device(win.device):
+        rc = lib.im2win_conv_f32(
+            win.data_ptr(), flt.data_ptr(), out.data_ptr(), n_img, c_in, params.c_out, h_out, w_out,
+            row_len, params.h_f, params.w_f, params.stride,
+            None if cplan is None else _byref(cplan), code, ws.data_ptr(), ws.numel(), stream)
+    _lib.check(rc)
+
+
+def _byref(x):
+    import ctypes
+
+    return ctypes.byref(x)
+
+
+def compute_from_windows_opt(windows: Im2winTensor, flt, params: ConvParams,
+                             plan: TilePlan | None = None, *, variant: str = "fp32-exact") -> Tensor4:
+    """Tiled convolution on an already-transformed input (optimized.py:217-234)."""
+    f = flt if isinstance(flt, Tensor4) else Tensor4(flt)
+    if f.dims != params.filter_dims:
+        raise ShapeError(f"filter dims {f.dims} do not match params {params.filter_dims}")
+    # the reference leaves these unchecked (optimized.py:217-226); a GPU kernel must not read out of bounds
+    if windows.c_in != params.c_in:
+        raise ShapeError(f"windows have {windows.c_in} channels, params expect {params.c_in}")
+    if (windows.h_f, windows.w_f, windows.stride) != (params.h_f, params.w_f, params.stride):
+        raise ShapeError("window tensor geometry does not match params")
+    fd = f.data if f.device == windows.data.device else f.data.to(windows.data.device)
+    # GemmDims is computed for parity with the reference call stack (optimized.py:222-223)
+    GemmDims(params.c_out, windows.n * windows.h_out * windows.w_out,
+             params.c_in * params.h_f * params.w_f)
+    out = torch.empty((windows.n, params.c_out, windows.h_out, windows.w_out), dtype=DTYPE,
+                      device=windows.data.device)
+    conv_windows_into(windows.data, fd, out, params, windows.w_eff, plan, variant)
+    return Tensor4(out)
+
+
+def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, *,
+                    variant: str = "fp32-exact") -> Tensor4:
+    """Window-order transform followed by the tiled kernel (optimized.py:237-241)."""
+    i = inp if isinstance(inp, Tensor4) else Tensor4(inp)
+    f = flt if isinstance(flt, Tensor4) else Tensor4(flt)
+    check_conv_operands(i, f, params)
+    return compute_from_windows_opt(im2win(i, params), f, params, plan, variant=variant)
