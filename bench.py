@@ -281,14 +281,14 @@ def main() -> None:
     sink = torch.empty(256, device=dev)
     peak = {}
     for exact in (1, 0):
-        iters, blocks = 4096, 148 * 8
-        lib.im2win_bench_fp32_peak(sink.data_ptr(), exact, 64, blocks, stream.cuda_stream)
+        iters, blocks = 1 << 15, 148 * 8
+        lib.im2win_bench_fp32_peak(sink.data_ptr(), exact, 256, blocks, stream.cuda_stream)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         lib.im2win_bench_fp32_peak(sink.data_ptr(), exact, iters, blocks, stream.cuda_stream)
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        peak["exact" if exact else "ffma"] = 2 * 16 * iters * 256 * blocks / (e0.elapsed_time(e1) * 1e-3) / 1e12
+        peak["exact" if exact else "ffma"] = 2 * 32 * iters * 256 * blocks / (e0.elapsed_time(e1) * 1e-3) / 1e12
 
     conv_flops = flops_step
     achieved = conv_flops / (conv_ms_total * 1e-3) / 1e12

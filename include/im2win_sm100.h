@@ -77,7 +77,7 @@ int im2win_conv_f32(const float* windows, const float* flt, float* out, int64_t 
                     void* workspace, size_t workspace_bytes, void* stream);
 
 /* Measurement utility (bench.py only): launches `blocks` x 256 threads that each
- * retire 2*16*iters flops of independent FP32 multiply-add chains; exact != 0
+ * retire 2*32*iters flops of independent FP32 multiply-add chains; exact != 0
  * issues FMUL+FADD (the conv's bit-exact pair), else FFMA.  Used to measure the
  * CUDA-core FP32 roofline denominator on the box (not in MEASURED_PEAKS.json). */
 int im2win_bench_fp32_peak(float* sink, int32_t exact, int32_t iters, int32_t blocks, void* stream);

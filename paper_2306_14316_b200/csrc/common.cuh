@@ -36,6 +36,14 @@ IM2WIN_DEVICE void cp_async_4(uint32_t dst, const void* src, uint32_t src_bytes)
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
 }
 
+// 4-byte async copy with an ignore-src predicate: zero-fills when `zero` is true.
+IM2WIN_DEVICE void cp_async_4_zfill(uint32_t dst, const void* src, bool zero) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+      "cp.async.ca.shared.global [%0], [%1], 4, p;\n\t}\n" ::"r"(dst),
+      "l"(src), "r"(static_cast<int>(zero)));
+}
+
 // 16-byte async copy (L2 only); src_bytes==0 zero-fills.
 IM2WIN_DEVICE void cp_async_16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));

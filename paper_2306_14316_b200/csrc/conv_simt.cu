@@ -19,7 +19,7 @@
 //   * the filter is pre-packed once per call into a zero-padded K-major panel
 //     FT[Kp][Mp] so its slabs are 16-byte async copies;
 //   * the window panel is gathered 4 bytes at a time with zero fill, using a
-//     per-k offset table delta[k] and per-column offsets col_off[n]
+//     per-k offset table delta[k] and per-column base pointers src_off(n)
 //     (the reference's hoisted src_off/delta, optimized.py:42, :101-102);
 //   * register micro-kernel: each thread owns an 8x8 tile split into two 4x4
 //     quadrants so fragments are 128-bit shared loads ("vectorized load").
@@ -32,7 +32,7 @@ struct ConvArgs {
   const float* __restrict__ fltT;   // packed filter [Kp][Mp]
   const int* __restrict__ delta;    // [Kp], -1 beyond K
   float* __restrict__ out;          // (N, Co, Ho, Wo)
-  int M, Mp, Kp;
+  int M, Mp, K, Kp;
   uint32_t n_gemm;                  // N*Ho*Wo
   uint32_t c_in, h_out, w_out, row_len, s_hf, hw;
   FastDiv fd_hw, fd_wo;
@@ -77,11 +77,12 @@ template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC>
 __global__ void __launch_bounds__((BM / 8) * (BN / 8), (BM * BN <= 128 * 128) ? 2 : 1)
     conv_simt_kernel(const ConvArgs a) {
   constexpr int NT = (BM / 8) * (BN / 8);
-  constexpr int TXN = BN / 8;  // threads along n
+  constexpr int TXN = BN / 8;                 // threads along n
+  constexpr int CPT = (BN + NT - 1) / NT;     // gather columns per thread
+  static_assert(BK % 4 == 0, "BK must be a multiple of 4 (int4 delta loads)");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* As = reinterpret_cast<float*>(smem_raw);                 // [STAGES][BK][BM]
-  float* Bs = As + STAGES * BK * BM;                              // [STAGES][BK][BN]
-  int64_t* col_off = reinterpret_cast<int64_t*>(Bs + STAGES * BK * BN);  // [BN]
+  float* As = reinterpret_cast<float*>(smem_raw);  // [STAGES][BK][BM]
+  float* Bs = As + STAGES * BK * BM;               // [STAGES][BK][BN]
 
   const int tid = threadIdx.x;
   const uint32_t m_tile = blockIdx.x % a.m_tiles;
@@ -89,21 +90,28 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), (BM * BN <= 128 * 128) ? 
   const int m0 = m_tile * BM;
   const uint32_t n0 = n_tile * BN;
 
-  for (int j = tid; j < BN; j += NT) {
-    uint32_t n = n0 + j;
-    int64_t off = -1;
-    if (n < a.n_gemm) {
+  // Per-thread gather columns: the window-matrix column n starts at
+  // src_off(n) = ((img*C*Ho + oh)*RL + ow*s*Hf) (optimized.py:101-102);
+  // element (k, n) is src_off(n) + delta[k].  Columns past N zero-fill.
+  const float* bsrc[CPT];
+  bool bzero[CPT];
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const uint32_t n = n0 + tid + j * NT;
+    bsrc[j] = a.win;
+    bzero[j] = true;
+    if (tid + j * NT < BN && n < a.n_gemm) {
       uint32_t img, rem, oh, ow;
       a.fd_hw.divmod(n, img, rem);
       a.fd_wo.divmod(rem, oh, ow);
-      off = (static_cast<int64_t>(img) * a.c_in * a.h_out + oh) * a.row_len +
-            static_cast<int64_t>(ow) * a.s_hf;
+      bsrc[j] = a.win + (static_cast<int64_t>(img) * a.c_in * a.h_out + oh) * a.row_len +
+                static_cast<int64_t>(ow) * a.s_hf;
+      bzero[j] = false;
     }
-    col_off[j] = off;
   }
-  __syncthreads();
 
   const int k_tiles = a.Kp / BK;
+  const int k_full = a.K / BK;  // slabs with no padded k
 
   auto load_stage = [&](int kt, int slot) {
     // filter slab: BK rows of BM floats, 16-byte copies
@@ -114,16 +122,30 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), (BM * BN <= 128 * 128) ? 
       int r = q / (BM / 4), c4 = q % (BM / 4);
       cp_async_16(smem_u32(adst + r * BM + c4 * 4), fsrc + static_cast<int64_t>(r) * a.Mp + c4 * 4, 16);
     }
-    // window slab: BK x BN gathered elements
-    float* bdst = Bs + slot * BK * BN;
+    // window slab: each gathering thread owns whole columns of BK elements
+    int d[BK];
 #pragma unroll
-    for (int q = tid; q < BK * BN; q += NT) {
-      int r = q / BN, c = q % BN;
-      int d = __ldg(a.delta + kt * BK + r);
-      int64_t co = col_off[c];
-      bool ok = (d >= 0) & (co >= 0);
-      const float* src = ok ? a.win + co + d : a.win;
-      cp_async_4(smem_u32(bdst + r * BN + c), src, ok ? 4u : 0u);
+    for (int q = 0; q < BK / 4; ++q) {
+      int4 v = __ldg(reinterpret_cast<const int4*>(a.delta + kt * BK) + q);
+      d[4 * q] = v.x; d[4 * q + 1] = v.y; d[4 * q + 2] = v.z; d[4 * q + 3] = v.w;
+    }
+    float* bdst = Bs + slot * BK * BN;
+    const bool full = kt < k_full;
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      const int c = tid + j * NT;
+      if (c < BN) {
+        if (full) {
+#pragma unroll
+          for (int kk = 0; kk < BK; ++kk) cp_async_4_zfill(smem_u32(bdst + kk * BN + c), bsrc[j] + d[kk], bzero[j]);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < BK; ++kk) {
+            const bool ok = d[kk] >= 0;
+            cp_async_4_zfill(smem_u32(bdst + kk * BN + c), ok ? bsrc[j] + d[kk] : a.win, bzero[j] || !ok);
+          }
+        }
+      }
     }
   };
 
@@ -230,7 +252,7 @@ static cudaError_t launch_cfg(const ConvArgs& a0, cudaStream_t stream) {
   a.m_tiles = (a.M + BM - 1) / BM;
   uint64_t n_tiles = (static_cast<uint64_t>(a.n_gemm) + BN - 1) / BN;
   uint64_t grid = n_tiles * a.m_tiles;
-  size_t smem = static_cast<size_t>(STAGES) * BK * (BM + BN) * 4 + BN * 8;
+  size_t smem = static_cast<size_t>(STAGES) * BK * (BM + BN) * 4;
   auto kern = conv_simt_kernel<BM, BN, BK, STAGES, EXACT, VEC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -255,7 +277,7 @@ extern "C" int im2win_simt_pick(int M, long long n_gemm, int K) {
 
 static const int kBM[] = {128, 64, 96, 128};
 static const int kBN[] = {128, 256, 128, 64};
-static const int kBK = 8;
+static const int kBK = 16;
 
 int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void* workspace,
                             int64_t n, int64_t c_in, int64_t c_out, int64_t h_out, int64_t w_out,
@@ -286,6 +308,7 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
   a.out = out;
   a.M = static_cast<int>(c_out);
   a.Mp = Mp;
+  a.K = static_cast<int>(K);
   a.Kp = Kp;
   a.n_gemm = static_cast<uint32_t>(n_gemm);
   a.c_in = static_cast<uint32_t>(c_in);
@@ -427,7 +450,7 @@ int im2win_launch_conv_simt_1x1(const float* win, const float* flt, float* out, 
                                               Kp, h_f, w_f, static_cast<int>(h_out * row_len));
   ConvArgs a{};
   a.win = win; a.fltT = fltT; a.delta = delta; a.out = out;
-  a.M = static_cast<int>(c_out); a.Mp = Mp; a.Kp = Kp;
+  a.M = static_cast<int>(c_out); a.Mp = Mp; a.K = static_cast<int>(K); a.Kp = Kp;
   a.n_gemm = static_cast<uint32_t>(n_gemm);
   a.c_in = static_cast<uint32_t>(c_in); a.h_out = static_cast<uint32_t>(h_out);
   a.w_out = static_cast<uint32_t>(w_out); a.row_len = static_cast<uint32_t>(row_len);

@@ -8,18 +8,19 @@ namespace im2win {
 
 template <bool EXACT>
 __global__ void __launch_bounds__(256) fp32_peak_kernel(float* sink, float a, float b, int iters) {
-  constexpr int C = 16;
+  constexpr int C = 32;
   float acc[C];
 #pragma unroll
   for (int j = 0; j < C; ++j) acc[j] = threadIdx.x * 1e-7f + j;
   float bb[C];
 #pragma unroll
   for (int j = 0; j < C; ++j) bb[j] = b + j * 1e-6f;
+  // each product depends on the running value, so nothing can be hoisted
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int j = 0; j < C; ++j) {
-      if constexpr (EXACT) acc[j] = __fadd_rn(acc[j], __fmul_rn(a, bb[j]));
-      else acc[j] = __fmaf_rn(a, bb[j], acc[j]);
+      if constexpr (EXACT) acc[j] = __fadd_rn(__fmul_rn(acc[j], a), bb[j]);
+      else acc[j] = __fmaf_rn(acc[j], a, bb[j]);
     }
   }
   float s = 0.f;
