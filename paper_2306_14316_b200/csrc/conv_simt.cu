@@ -74,7 +74,7 @@ IM2WIN_DEVICE float mac(float acc, float a, float b) {
 }
 
 template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC>
-__global__ void __launch_bounds__((BM / 8) * (BN / 8), (BM * BN <= 128 * 128) ? 2 : 1)
+__global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
     conv_simt_kernel(const ConvArgs a) {
   constexpr int NT = (BM / 8) * (BN / 8);
   constexpr int TXN = BN / 8;                 // threads along n
@@ -275,9 +275,13 @@ extern "C" int im2win_simt_pick(int M, long long n_gemm, int K) {
   return 0;                 // 128 x 128
 }
 
-static const int kBM[] = {128, 64, 96, 128};
-static const int kBN[] = {128, 256, 128, 64};
-static const int kBK = 16;
+// Compiled CTA tiles (index = im2win_tile_plan.block_cfg).  0-3 are the
+// production tiles (all toggles compiled); 4+ are exploration tiles.
+static const int kNumCfg = 7;
+static const int kBM[kNumCfg] = {128, 64, 96, 128, 64, 128, 64};
+static const int kBN[kNumCfg] = {128, 256, 128, 64, 256, 128, 256};
+static const int kBKc[kNumCfg] = {16, 16, 16, 16, 32, 32, 16};
+static const int kMaxBK = 32;
 
 int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void* workspace,
                             int64_t n, int64_t c_in, int64_t c_out, int64_t h_out, int64_t w_out,
@@ -292,10 +296,14 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
     return 1;
   }
   if (cfg < 0) cfg = im2win_simt_pick(static_cast<int>(c_out), n_gemm, static_cast<int>(K));
-  const int BM = kBM[cfg], BN = kBN[cfg];
-  (void)BN;
+  if (cfg >= kNumCfg) {
+    *err = "im2win_conv_f32: unknown tile configuration";
+    return 1;
+  }
+  if (cfg >= 4 && !(exact && vec && stages > 1)) cfg = im2win_simt_pick(static_cast<int>(c_out), n_gemm, static_cast<int>(K));
+  const int BM = kBM[cfg], BK = kBKc[cfg];
   const int Mp = static_cast<int>((c_out + BM - 1) / BM * BM);
-  const int Kp = static_cast<int>((K + kBK - 1) / kBK * kBK);
+  const int Kp = static_cast<int>((K + BK - 1) / BK * BK);
   float* fltT = static_cast<float*>(workspace);
   int* delta = reinterpret_cast<int*>(fltT + static_cast<int64_t>(Kp) * Mp);
 
@@ -321,16 +329,19 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
   a.fd_wo = FastDiv(static_cast<uint32_t>(w_out));
 
   cudaError_t e = cudaSuccess;
-#define IM2WIN_DISPATCH(BM_, BN_)                                                                  \
-  if (exact && vec && stages == 3) e = launch_cfg<BM_, BN_, kBK, 3, true, true>(a, stream);         \
-  else if (exact && vec && stages == 1) e = launch_cfg<BM_, BN_, kBK, 1, true, true>(a, stream);    \
-  else if (exact && !vec) e = launch_cfg<BM_, BN_, kBK, 3, true, false>(a, stream);                 \
-  else e = launch_cfg<BM_, BN_, kBK, 3, false, true>(a, stream);
+#define IM2WIN_DISPATCH(BM_, BN_, BK_)                                                              \
+  if (exact && vec && stages == 3) e = launch_cfg<BM_, BN_, BK_, 3, true, true>(a, stream);          \
+  else if (exact && vec && stages == 1) e = launch_cfg<BM_, BN_, BK_, 1, true, true>(a, stream);     \
+  else if (exact && !vec) e = launch_cfg<BM_, BN_, BK_, 3, true, false>(a, stream);                  \
+  else e = launch_cfg<BM_, BN_, BK_, 3, false, true>(a, stream);
   switch (cfg) {
-    case 0: { IM2WIN_DISPATCH(128, 128) break; }
-    case 1: { IM2WIN_DISPATCH(64, 256) break; }
-    case 2: { IM2WIN_DISPATCH(96, 128) break; }
-    case 3: { IM2WIN_DISPATCH(128, 64) break; }
+    case 0: { IM2WIN_DISPATCH(128, 128, 16) break; }
+    case 1: { IM2WIN_DISPATCH(64, 256, 16) break; }
+    case 2: { IM2WIN_DISPATCH(96, 128, 16) break; }
+    case 3: { IM2WIN_DISPATCH(128, 64, 16) break; }
+    case 4: e = launch_cfg<64, 256, 32, 2, true, true>(a, stream); break;
+    case 5: e = launch_cfg<128, 128, 32, 2, true, true>(a, stream); break;
+    case 6: e = launch_cfg<64, 256, 16, 4, true, true>(a, stream); break;
     default: *err = "im2win_conv_f32: unknown tile configuration"; return 1;
   }
 #undef IM2WIN_DISPATCH
@@ -344,7 +355,7 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
 // Workspace needed by im2win_launch_conv_simt for any configuration.
 size_t im2win_simt_workspace_bytes(int64_t c_out, int64_t K) {
   const int64_t Mp = (c_out + 127) / 128 * 128 + 128;
-  const int64_t Kp = (K + kBK - 1) / kBK * kBK;
+  const int64_t Kp = (K + kMaxBK - 1) / kMaxBK * kMaxBK;
   return static_cast<size_t>(Kp * Mp) * 4 + static_cast<size_t>(Kp) * 4 + 256;
 }
 
