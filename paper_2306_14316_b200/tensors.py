@@ -38,10 +38,10 @@ def _to_device_f32(data, ndim: int, device=None) -> torch.Tensor:
     if data.dtype != DTYPE:
         data = data.to(DTYPE)
     if not data.is_cuda:
-        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        data = data.pin_memory().to(dev, non_blocking=True) if torch.cuda.is_available() else data
-        if not data.is_cuda:
+        if not torch.cuda.is_available():
             raise ShapeError("a CUDA device is required (this package has no CPU path)")
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        data = data.to(dev)
     return data.contiguous()
 
 

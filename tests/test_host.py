@@ -1,0 +1,124 @@
+"""Host-side logic (no GPU): geometry, plans, errors, footprints, fixtures, the C-ABI library."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2306_14316_b200 as pkg
+from paper_2306_14316_b200 import _lib
+from paper_2306_14316_b200.plan import simt_tile_for, to_c_plan
+
+ROOT = Path(__file__).resolve().parent.parent
+
+# pkg/tests/test_acceptance.py:24-37 (paper Table 2)
+TABLE2_OUTPUTS = {
+    "conv1": (96, 55, 55), "conv2": (96, 56, 56), "conv3": (64, 111, 111), "conv4": (64, 109, 109),
+    "conv5": (256, 20, 20), "conv6": (512, 10, 10), "conv7": (64, 222, 222), "conv8": (128, 110, 110),
+    "conv9": (64, 54, 54), "conv10": (128, 26, 26), "conv11": (256, 12, 12), "conv12": (512, 5, 5),
+}
+
+
+def test_table2_geometry():
+    for name, cfg in pkg.BENCHMARKS.items():
+        assert (cfg.c_out, *cfg.out_dims) == TABLE2_OUTPUTS[name], name
+
+
+def test_flops_formula():
+    cfg = pkg.BENCHMARKS["conv1"]
+    assert cfg.flops == 2 * 2 * 96 * 55 * 55 * 3 * 11 * 11
+
+
+def test_conv_params_validation():
+    with pytest.raises(pkg.GeometryError):
+        pkg.ConvParams(0, 1, 3, 3, 1)
+    with pytest.raises(pkg.GeometryError):
+        pkg.ConvParams(1, 1, 3, 3, 0)
+    with pytest.raises(pkg.GeometryError):
+        pkg.output_dims(2, 5, pkg.ConvParams(1, 1, 3, 3, 1))
+    assert pkg.output_dims(224, 224, pkg.ConvParams(64, 64, 7, 7, 2)) == (109, 109)
+    assert pkg.effective_width(109, 7, 2) == 223
+
+
+def test_tile_plan_validation():
+    with pytest.raises(pkg.PlanError):
+        pkg.TilePlan(m_b=6, n_b=8, k_b=4, m_t=4, n_t=2)
+    with pytest.raises(pkg.PlanError):
+        pkg.TilePlan(m_b=0, n_b=8, k_b=4, m_t=1, n_t=2)
+    plan = pkg.TilePlan(m_b=8, n_b=8, k_b=4, m_t=4, n_t=4, micro_kernel=False)
+    assert (plan.m_t, plan.n_t) == (1, 1) and plan.workers_per_block == 64
+    for cfg in pkg.BENCHMARKS.values():
+        p = pkg.default_plan(cfg.gemm_dims())
+        assert p.m_b % p.m_t == 0 and p.n_b % p.n_t == 0
+    assert pkg.default_plan(pkg.GemmDims(1, 500, 64)).m_b == 1
+
+
+def test_plan_to_c_abi():
+    assert to_c_plan(None) is None
+    c = to_c_plan(pkg.TilePlan(64, 256, 16, 8, 8))
+    assert (c.block_cfg, c.micro_kernel, c.vectorized_load, c.prefetch_double_buffer) == (1, 1, 1, 1)
+    c = to_c_plan(pkg.TilePlan(64, 128, 128, 8, 8, prefetch_double_buffer=False, vectorized_load=False))
+    assert (c.block_cfg, c.vectorized_load, c.prefetch_double_buffer) == (-1, 0, 0)
+    c = to_c_plan(pkg.TilePlan(64, 128, 128, 8, 8, micro_kernel=False))
+    assert c.micro_kernel == 0
+    assert pkg.gpu_plan(pkg.BENCHMARKS["conv4"].gemm_dims()).m_b == 64
+    assert simt_tile_for(pkg.GemmDims(96, 10 ** 6, 363)) == 2
+
+
+def test_gemm_index_roundtrip():
+    for n in range(0, 2 * 5 * 7):
+        assert pkg.compose_n(*pkg.decompose_n(n, 5, 7), 5, 7) == n
+    for k in range(0, 3 * 4 * 5):
+        assert pkg.compose_k(*pkg.decompose_k(k, 4, 5), 4, 5) == k
+
+
+def test_footprints_match_reference_counts():
+    p = pkg.ConvParams(3, 96, 11, 11, 4)
+    assert pkg.footprint_elems("im2col", 1, 3, 227, 227, p) == 1_098_075
+    assert pkg.footprint_elems("im2win", 1, 3, 227, 227, p) == 412_005
+    assert pkg.footprint_elems("raw", 1, 3, 227, 227, p) == 154_587
+    f1 = pkg.ConvParams(3, 2, 2, 2, 1)
+    assert [pkg.footprint_elems(l, 1, 3, 3, 3, f1) for l in ("raw", "im2col", "im2win")] == [27, 48, 36]
+    with pytest.raises(ValueError):
+        pkg.footprint_elems("nchw", 1, 3, 3, 3, f1)
+
+
+def test_max_rel_diff_semantics():
+    a = np.array([[[[1.0, -0.0, np.nan, 10.0]]]], np.float32)
+    b = np.array([[[[1.0, 0.0, np.nan, 11.0]]]], np.float32)
+    assert pkg.max_rel_diff(a, a) == 0.0
+    assert pkg.max_rel_diff(a[..., :2], b[..., :2]) == 0.0   # |diff|=0 for +-0
+    assert abs(pkg.max_rel_diff(a[..., 3:], b[..., 3:]) - 1 / 11) < 1e-12
+    with pytest.raises(pkg.ShapeError):
+        pkg.max_rel_diff(a, b[..., :2])
+
+
+def test_fixture_roundtrip(tmp_path):
+    x = np.random.default_rng(0).standard_normal((1, 2, 3, 4)).astype(np.float32)
+    x[0, 0, 0, 0] = np.nan
+    x[0, 0, 0, 1] = -0.0
+    pkg.write_tensor(x, tmp_path / "a.wct4")
+    y = pkg.read_tensor(tmp_path / "a.wct4")
+    assert (x.view(np.uint32) == y.view(np.uint32)).all()
+    (tmp_path / "bad").write_bytes(b"XXXX" + bytes(40))
+    with pytest.raises(pkg.FixtureFormatError):
+        pkg.read_tensor(tmp_path / "bad")
+
+
+def test_c_abi_library_exports_every_header_symbol():
+    header = (ROOT / "include" / "im2win_sm100.h").read_text()
+    declared = set(re.findall(r"^\s*(?:int|size_t|const char\*|int32_t)\s+(im2win_\w+)\s*\(", header, re.M))
+    assert declared == set(_lib.EXPORTED_SYMBOLS)
+    lib = _lib.load()
+    for sym in declared:
+        assert hasattr(lib, sym), sym
+    assert lib.im2win_abi_version() == 100
+    assert lib.im2win_conv_workspace_bytes(64, 64, 3, 3, 0) > 64 * 64 * 9 * 4
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback():
+    with pytest.raises(pkg.ShapeError, match="CUDA"):
+        pkg.Tensor4(np.zeros((1, 1, 4, 4), np.float32))
