@@ -268,52 +268,99 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= kProducerWarp0) {
     // ---------------- window-tile producers: Ĩ -> swizzled A stage ----------------
-    const int pw = warp - kProducerWarp0;        // rows [16*pw, 16*pw + 16)
+    // Warp pw owns A rows [16*pw, 16*pw+16) of every tile; lane = position in the
+    // 128-byte K row.  Row r, K-byte b lives at (r/8)*1024 + (r%8)*128 + ((b/16)^(r%8))*16 + b%16
+    // (UMMA K-major SWIZZLE_128B canonical layout).
+    const int pw = warp - kProducerWarp0;
     constexpr int kRows = kTileM / kProducerWarps;
-    uint32_t stage = 0, phase = 0;
-    for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      const uint32_t pix_blk = t / a.co_tiles;
-      // lane l < 16 owns the source offset of row 16*pw + l
-      int64_t my_off = -1;
+    auto row_offset = [&](uint32_t t) -> int64_t {
+      int64_t off = -1;
       if (lane < kRows) {
-        const uint32_t n = pix_blk * kTileM + pw * kRows + lane;
+        const uint32_t n = (t / a.co_tiles) * kTileM + pw * kRows + lane;
         if (n < a.n_gemm) {
           uint32_t img, rem, oh, ow;
           a.fd_hw.divmod(n, img, rem);
           a.fd_wo.divmod(rem, oh, ow);
-          my_off = (static_cast<int64_t>(img) * a.c_in * a.h_out + oh) * a.row_len + static_cast<int64_t>(ow) * a.s_hf;
+          off = (static_cast<int64_t>(img) * a.c_in * a.h_out + oh) * a.row_len + static_cast<int64_t>(ow) * a.s_hf;
         }
       }
-      for (uint32_t ks = 0; ks < a.k_slabs; ++ks) {
-        int d0, d1 = -1;
-        if constexpr (BF16) {
-          int2 dd = __ldg(reinterpret_cast<const int2*>(a.delta + ks * kBK) + lane);
-          d0 = dd.x;
-          d1 = dd.y;
-        } else {
-          d0 = __ldg(a.delta + ks * kBK + lane);
+      return off;
+    };
+    auto a_slot = [&](uint32_t stage_idx, int i) -> uint8_t* {
+      const int r = pw * kRows + i;
+      const uint32_t chunk = (static_cast<uint32_t>(lane) >> 2) ^ (r & 7);
+      return smem + stage_idx * kStageBytes + (r >> 3) * 1024 + (r & 7) * 128 + chunk * 16 + (lane & 3) * 4;
+    };
+    if constexpr (!BF16) {
+      // TF32: 4-byte cp.async straight into the swizzled slot (tf32 = fp32 bits, the
+      // tensor core ignores the low mantissa: round-toward-zero); D slabs in flight per warp.
+      constexpr int D = STAGES >= 5 ? 4 : STAGES - 1;
+      uint32_t stage = 0, phase = 0, rstage = 0, unretired = 0;
+      for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const int64_t my_off = row_offset(t);
+        for (uint32_t ks = 0; ks < a.k_slabs; ++ks) {
+          const int d = __ldg(a.delta + ks * kBK + lane);
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+#pragma unroll
+          for (int i = 0; i < kRows; ++i) {
+            const int64_t off = __shfl_sync(0xffffffffu, my_off, i);
+            const bool zero = off < 0 || d < 0;
+            cp_async_4_zfill(smem_u32(a_slot(stage, i)), zero ? a.win : a.win + off + d, zero);
+          }
+          cp_async_commit();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++unretired == D + 1) {
+            cp_async_wait<D>();
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full_bar[rstage]);
+            if (++rstage == STAGES) rstage = 0;
+            --unretired;
+          }
         }
-        float v0[kRows], v1[kRows];
+      }
+      cp_async_wait<0>();
+      fence_proxy_async_smem();
+      __syncwarp();
+      for (; unretired > 0; --unretired) {
+        if (lane == 0) mbar_arrive(&full_bar[rstage]);
+        if (++rstage == STAGES) rstage = 0;
+      }
+    } else {
+      // BF16: registers (fp32 -> bf16x2), software pipelined one slab ahead.
+      uint32_t stage = 0, phase = 0;
+      uint32_t t = blockIdx.x, ks = 0;
+      int64_t my_off = t < total_tiles ? row_offset(t) : -1;
+      float c0[kRows], c1[kRows];
+      auto load = [&](uint32_t kslab, int64_t off_reg, float (&v0)[kRows], float (&v1)[kRows]) {
+        const int2 dd = __ldg(reinterpret_cast<const int2*>(a.delta + kslab * kBK) + lane);
 #pragma unroll
         for (int i = 0; i < kRows; ++i) {
-          const int64_t off = __shfl_sync(0xffffffffu, my_off, i);
-          v0[i] = (off >= 0 && d0 >= 0) ? __ldg(a.win + off + d0) : 0.0f;
-          if constexpr (BF16) v1[i] = (off >= 0 && d1 >= 0) ? __ldg(a.win + off + d1) : 0.0f;
+          const int64_t off = __shfl_sync(0xffffffffu, off_reg, i);
+          v0[i] = (off >= 0 && dd.x >= 0) ? __ldg(a.win + off + dd.x) : 0.0f;
+          v1[i] = (off >= 0 && dd.y >= 0) ? __ldg(a.win + off + dd.y) : 0.0f;
+        }
+      };
+      if (t < total_tiles) load(0, my_off, c0, c1);
+      while (t < total_tiles) {
+        uint32_t nt = t, nks = ks + 1;
+        if (nks == a.k_slabs) { nks = 0; nt += gridDim.x; }
+        float n0[kRows], n1[kRows];
+        if (nt < total_tiles) {
+          if (nt != t) my_off = row_offset(nt);
+          load(nks, my_off, n0, n1);
         }
         mbar_wait(&empty_bar[stage], phase ^ 1);
-        uint8_t* adst = smem + stage * kStageBytes;
 #pragma unroll
-        for (int i = 0; i < kRows; ++i) {
-          const int r = pw * kRows + i;
-          const uint32_t chunk = (static_cast<uint32_t>(lane) >> 2) ^ (r & 7);
-          uint32_t* p = reinterpret_cast<uint32_t*>(adst + (r >> 3) * 1024 + (r & 7) * 128 + chunk * 16 + (lane & 3) * 4);
-          if constexpr (BF16) *p = pack_bf16x2(v0[i], v1[i]);
-          else *p = to_tf32(v0[i]);
-        }
+        for (int i = 0; i < kRows; ++i) *reinterpret_cast<uint32_t*>(a_slot(stage, i)) = pack_bf16x2(c0[i], c1[i]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&full_bar[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) { c0[i] = n0[i]; c1[i] = n1[i]; }
+        t = nt;
+        ks = nks;
       }
     }
   }

@@ -129,3 +129,45 @@ def test_errors_raise_before_launch():
         pkg.im2win(x, pkg.ConvParams(3, 1, 9, 3, 1))
     with pytest.raises(pkg.ShapeError):
         pkg.conv_im2win_opt(x, torch.randn(2, 3, 3, 3, device=DEV), pkg.ConvParams(3, 1, 3, 3, 1))
+
+
+# ---------------------------------------------------------------- tensor-core variants
+# Stated tolerances: normalized max|d|/rms(ref)
+# TF32 <= 1e-2, BF16 <= 4e-2 (operands rounded to nearest, fp32 accumulation).
+TC_TOL = {"tf32": 1e-2, "bf16": 4e-2}
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+@pytest.mark.parametrize("name", list(BENCHMARKS))
+def test_tc_layers_within_tolerance(name, variant, layer_goldens):
+    g = layer_goldens[name]
+    cfg = replace(BENCHMARKS[name], batch=g["batch"], seed=g["seed"])
+    inp, flt = make_inputs(cfg)
+    out = pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant).numpy()
+    ref = orc.conv_direct(inp, flt, cfg.stride)
+    assert orc.checksum(ref) == g["out_sha"]
+    assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], name
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_tc_small_cases(small_cases, variant):
+    for name, c in small_cases.items():
+        if name == "special":
+            continue
+        out = pkg.conv_im2win_opt(torch.from_numpy(c["inp"]).to(DEV), torch.from_numpy(c["flt"]).to(DEV),
+                                  _params(c), variant=variant).numpy()
+        ref = c["out"]
+        err = np.max(np.abs(out.astype(np.float64) - ref)) / max(np.sqrt(np.mean(ref.astype(np.float64) ** 2)), 1e-3)
+        assert err <= 2 * TC_TOL[variant], (name, err)
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_tc_large_batch_sampled_images(variant):
+    cfg = replace(BENCHMARKS["conv8"], batch=128, seed=11)
+    g = torch.Generator(device="cpu").manual_seed(11)
+    inp = torch.randn((cfg.batch, cfg.c_in, cfg.h_in, cfg.w_in), generator=g)
+    flt = torch.randn((cfg.c_out, cfg.c_in, cfg.h_f, cfg.w_f), generator=g)
+    out = pkg.conv_im2win_opt(inp.to(DEV), flt.to(DEV), cfg.params, variant=variant)
+    for i in (0, 77, 127):
+        ref = orc.conv_direct(inp[i:i + 1].numpy(), flt.numpy(), cfg.stride)
+        assert pkg.normalized_max_diff(out.data[i:i + 1].cpu().numpy(), ref) <= TC_TOL[variant]
