@@ -76,6 +76,23 @@ int im2win_conv_f32(const float* windows, const float* flt, float* out, int64_t 
                     int32_t w_f, int32_t stride, const im2win_tile_plan* plan, int32_t variant,
                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Tensor-core fast path (extension; no counterpart in the reference) ----
+ * The channels-innermost form of the window layout, Ĩcl[n*Ho+oh][col][fh][c] =
+ * X[n][c][oh*stride+fh][col] (col < w_eff), makes every pixel's window one
+ * contiguous run of c_in*h_f*w_f elements, so the tcgen05 kernel streams window
+ * tiles with TMA and no gather.  dtype 0 stores float32 (TF32 variant), 1 bf16.
+ * Requires c_in * element size to be a multiple of 16 bytes for im2win_conv_cl. */
+int im2win_transform_cl(const float* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w,
+                        int32_t h_f, int32_t w_f, int32_t stride, int32_t dtype, void* stream);
+
+size_t im2win_conv_cl_workspace_bytes(int64_t c_in, int64_t c_out, int32_t h_f, int32_t w_f);
+
+/* variant = IM2WIN_TF32 (windows_cl float32) or IM2WIN_BF16 (windows_cl bf16). */
+int im2win_conv_cl(const void* windows_cl, const float* flt, float* out, int64_t n, int64_t c_in,
+                   int64_t c_out, int64_t h_out, int64_t w_out, int32_t h_f, int32_t w_f,
+                   int32_t stride, int32_t variant, void* workspace, size_t workspace_bytes,
+                   void* stream);
+
 /* Measurement utility (bench.py only): launches `blocks` x 256 threads that each
  * retire 2*32*iters flops of independent FP32 multiply-add chains; exact != 0
  * issues FMUL+FADD (the conv's bit-exact pair), else FFMA.  Used to measure the

@@ -30,6 +30,9 @@ EXPORTED_SYMBOLS = (
     "im2win_last_error",
     "im2win_abi_version",
     "im2win_bench_fp32_peak",
+    "im2win_transform_cl",
+    "im2win_conv_cl_workspace_bytes",
+    "im2win_conv_cl",
 )
 
 
@@ -73,6 +76,12 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         lib.im2win_abi_version.restype = ctypes.c_int32
         lib.im2win_bench_fp32_peak.argtypes = [vp, i32, i32, i32, vp]
         lib.im2win_bench_fp32_peak.restype = ctypes.c_int
+        lib.im2win_transform_cl.argtypes = [vp, vp, i64, i64, i64, i64, i32, i32, i32, i32, vp]
+        lib.im2win_transform_cl.restype = ctypes.c_int
+        lib.im2win_conv_cl_workspace_bytes.argtypes = [i64, i64, i32, i32]
+        lib.im2win_conv_cl_workspace_bytes.restype = sz
+        lib.im2win_conv_cl.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32, i32, vp, sz, vp]
+        lib.im2win_conv_cl.restype = ctypes.c_int
         if path is None:
             _lib = lib
         return lib

@@ -1,0 +1,405 @@
+// Channels-innermost im2win + TMA-fed tcgen05 convolution (the tensor-core fast path).
+//
+// Layout Ĩcl (internal; the NHWC form of the im2win window layout): for output row
+// g = img*Ho + oh, source column col < w_eff, filter row fh < Hf and channel c < C
+//     Ĩcl[g][col][fh][c] = X[img][c][oh*s + fh][col]
+// It is the reference's window order (layouts.py:73-83: per output row, the Hf input
+// rows it touches, column by column, the Hf values of a column contiguous) with the
+// channel moved innermost.  A pixel's whole dot-product window is then ONE contiguous
+// run of K = Wf*Hf*C elements starting at Ĩcl[g][ow*s][0][0], and consecutive pixels of
+// a row are s*Hf*C elements apart, so the GEMM operand
+//     A[(g, ow)][k'] = Ĩcl[g*RLc + ow*s*Hf*C + k'],  k' = (fw*Hf + fh)*C + c
+// is a strided 3-D view {k', ow, g} that a TMA tensor map walks directly (the windows
+// overlap in memory; TMA only reads).  No gather, no repack: TMA delivers 128-byte
+// swizzled K-major tiles that tcgen05.mma consumes as-is, K and pixel tails are
+// zero-filled by TMA's out-of-bounds handling.
+//
+// Tile = box_g output rows x box_w output columns (<= 128 pixels = UMMA M rows),
+// Co tile = UMMA N.  Warp 0: TMA producer (A + filter B), warp 1: MMA issuer,
+// warp 2: TMEM allocator, warps 4-7: epilogue (TMEM -> NCHW, coalesced along ow).
+#include <stddef.h>
+#include <stdint.h>
+
+#include "tc_common.cuh"
+
+namespace im2win {
+namespace tc {
+
+// ---------------------------------------------------------------- transform
+// CTA = (g, fh, 32 columns, 32 channels); smem transpose (c <-> col).
+template <bool BF16>
+__global__ void __launch_bounds__(256) transform_cl_kernel(const float* __restrict__ src, void* __restrict__ dst,
+                                                           uint32_t c_in, uint32_t h_in, uint32_t w_in,
+                                                           uint32_t h_out, uint32_t h_f, uint32_t stride,
+                                                           uint32_t w_eff, uint32_t col_blocks, uint32_t c_blocks,
+                                                           uint32_t total_blocks) {
+  __shared__ float tile[32][33];
+  const uint32_t tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  for (uint32_t b = blockIdx.x; b < total_blocks; b += gridDim.x) {
+    uint32_t rest = b;
+    const uint32_t cb = rest % c_blocks;
+    rest /= c_blocks;
+    const uint32_t colb = rest % col_blocks;
+    rest /= col_blocks;
+    const uint32_t fh = rest % h_f;
+    const uint32_t g = rest / h_f;
+    const uint32_t img = g / h_out, oh = g % h_out;
+    const uint32_t col0 = colb * 32, c0 = cb * 32;
+    const uint32_t row = oh * stride + fh;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t c = c0 + ty + 8 * j, col = col0 + tx;
+      float v = 0.0f;
+      if (c < c_in && col < w_eff) v = __ldg(src + ((static_cast<uint64_t>(img) * c_in + c) * h_in + row) * w_in + col);
+      tile[ty + 8 * j][tx] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t col = col0 + ty + 8 * j, c = c0 + tx;
+      if (c < c_in && col < w_eff) {
+        const uint64_t o = ((static_cast<uint64_t>(g) * w_eff + col) * h_f + fh) * c_in + c;
+        if constexpr (BF16) reinterpret_cast<__nv_bfloat16*>(dst)[o] = __float2bfloat16_rn(tile[tx][ty + 8 * j]);
+        else reinterpret_cast<float*>(dst)[o] = tile[tx][ty + 8 * j];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- GEMM
+struct ClArgs {
+  float* __restrict__ out;  // (N, Co, Ho, Wo)
+  uint32_t g_total;         // N*Ho
+  uint32_t h_out, w_out, hw, co;
+  uint32_t box_w, box_g;    // pixel tile = box_g rows x box_w columns
+  uint32_t ow_tiles, g_tiles, co_tiles;
+  uint32_t k_slabs;
+};
+
+template <bool BF16, int N, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+    conv_tc_cl_kernel(const ClArgs a, const __grid_constant__ CUtensorMap tmap_a,
+                      const __grid_constant__ CUtensorMap tmap_b) {
+  constexpr uint32_t kABytes = kTileM * kRowBytes;
+  constexpr uint32_t kBBytes = N * kRowBytes;
+  constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  constexpr int kBK = BF16 ? 64 : 32;
+  constexpr int kUK = BF16 ? 16 : 8;
+  constexpr uint32_t kTmemCols = (2 * N <= 128) ? 128 : (2 * N <= 256 ? 256 : 512);
+  constexpr uint32_t kIdesc = instr_desc<BF16, N>();
+
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t tfull_bar[2];
+  __shared__ __align__(8) uint64_t tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t a_box_bytes = a.box_w * a.box_g * kRowBytes;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);
+    }
+    fence_barrier_init();
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap_b) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+  const uint32_t total_tiles = a.g_tiles * a.ow_tiles * a.co_tiles;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const uint32_t co_blk = t % a.co_tiles;
+        const uint32_t pt = t / a.co_tiles;
+        const uint32_t ow0 = (pt % a.ow_tiles) * a.box_w;
+        const uint32_t g0 = (pt / a.ow_tiles) * a.box_g;
+        for (uint32_t ks = 0; ks < a.k_slabs; ++ks) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* st = smem + stage * kStageBytes;
+          mbar_arrive_expect_tx(&full_bar[stage], a_box_bytes + kBBytes);
+          tma_load_3d(st, &tmap_a, &full_bar[stage], ks * kBK, ow0, g0);
+          tma_load_2d(st + kABytes, &tmap_b, &full_bar[stage], ks * kBK, co_blk * N);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * N;
+        for (uint32_t ks = 0; ks < a.k_slabs; ++ks) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t abase = smem_u32(smem + stage * kStageBytes);
+          const uint32_t bbase = abase + kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / kUK; ++kk)
+            mma<BF16>(tmem_d, smem_desc_sw128(abase + kk * 32), smem_desc_sw128(bbase + kk * 32), kIdesc,
+                      (ks | kk) != 0);
+          mma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull_bar[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int quarter = warp % 4;
+    const uint32_t r = quarter * 32 + lane;  // A row = TMEM lane
+    const uint32_t rg = r / a.box_w, rw = r % a.box_w;
+    uint32_t acc = 0, acc_phase = 0;
+    for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const uint32_t co_blk = t % a.co_tiles;
+      const uint32_t pt = t / a.co_tiles;
+      const uint32_t ow = (pt % a.ow_tiles) * a.box_w + rw;
+      const uint32_t g = (pt / a.ow_tiles) * a.box_g + rg;
+      const bool valid = rg < a.box_g && ow < a.w_out && g < a.g_total;
+      int64_t obase = 0;
+      if (valid) {
+        const uint32_t img = g / a.h_out, oh = g % a.h_out;
+        obase = static_cast<int64_t>(img) * a.co * a.hw + static_cast<int64_t>(oh) * a.w_out + ow;
+      }
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * N;
+#pragma unroll
+      for (int j0 = 0; j0 < N; j0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(taddr + j0, v);
+        const uint32_t m0 = co_blk * N + j0;
+        if (valid) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (m0 + q < a.co) a.out[obase + static_cast<int64_t>(m0 + q) * a.hw] = __uint_as_float(v[q]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(kTmemCols));
+  }
+}
+
+// B[m][k'] = F[m][c][fh][fw], k' = (fw*Hf + fh)*C + c, zero padded to Mp x Kp.
+template <bool BF16>
+__global__ void pack_filter_cl_kernel(const float* __restrict__ flt, void* __restrict__ packed, int M, int C, int h_f,
+                                      int w_f, int Mp, int Kp) {
+  const int K = C * h_f * w_f;
+  const int64_t total = static_cast<int64_t>(Mp) * Kp;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(i / Kp);
+    const int kp = static_cast<int>(i % Kp);
+    float v = 0.0f;
+    if (m < M && kp < K) {
+      const int c = kp % C, j = kp / C;
+      const int fw = j / h_f, fh = j % h_f;
+      v = flt[((static_cast<int64_t>(m) * C + c) * h_f + fh) * w_f + fw];
+    }
+    if constexpr (BF16) {
+      reinterpret_cast<__nv_bfloat16*>(packed)[i] = __float2bfloat16_rn(v);
+    } else {
+      uint32_t r;
+      asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(v));
+      reinterpret_cast<uint32_t*>(packed)[i] = r;
+    }
+  }
+}
+
+static int pick_n_cl(int64_t co) {
+  if (co <= 64) return 64;
+  if (co <= 96) return 96;
+  if (co <= 128) return 128;
+  return 256;
+}
+
+template <bool BF16, int N, int STAGES>
+static int launch_cl(ClArgs a, const void* win_cl, const void* packed, int64_t K, int64_t Kp, int64_t Mp,
+                     int64_t c_in, int32_t h_f, int32_t stride, int64_t w_eff, cudaStream_t stream, const char** err) {
+  constexpr int kBK = BF16 ? 64 : 32;
+  auto enc = get_encode_fn();
+  if (!enc) {
+    *err = "conv_tc_cl: cuTensorMapEncodeTiled unavailable";
+    return 2;
+  }
+  const cuuint64_t esz = BF16 ? 2 : 4;
+  const CUtensorMapDataType dt = BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUtensorMap map_a, map_b;
+  {
+    // A: {k' < K, ow < Wo, g < N*Ho}; pixel stride s*Hf*C, row stride w_eff*Hf*C (windows overlap)
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), a.w_out, a.g_total};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(stride) * h_f * c_in * esz,
+                             static_cast<cuuint64_t>(w_eff) * h_f * c_in * esz};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), a.box_w, a.box_g};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(&map_a, dt, 3, const_cast<void*>(win_cl), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      *err = "conv_tc_cl: window tensor map rejected (cuTensorMapEncodeTiled)";
+      return 2;
+    }
+  }
+  {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(Mp)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(Kp) * esz};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(N)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&map_b, dt, 2, const_cast<void*>(packed), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      *err = "conv_tc_cl: filter tensor map rejected (cuTensorMapEncodeTiled)";
+      return 2;
+    }
+  }
+  a.k_slabs = static_cast<uint32_t>(Kp / kBK);
+  a.co_tiles = static_cast<uint32_t>(Mp / N);
+  const size_t smem = static_cast<size_t>(STAGES) * (kTileM + N) * kRowBytes + 1024;
+  auto kern = conv_tc_cl_kernel<BF16, N, STAGES>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 2;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t tiles = static_cast<uint64_t>(a.g_tiles) * a.ow_tiles * a.co_tiles;
+  const uint32_t grid = tiles < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(tiles) : static_cast<uint32_t>(sms);
+  kern<<<grid, 256, smem, stream>>>(a, map_a, map_b);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 2;
+  }
+  return 0;
+}
+
+}  // namespace tc
+}  // namespace im2win
+
+int im2win_launch_transform_cl(const float* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w, int h_f,
+                               int w_f, int stride, int bf16, cudaStream_t stream, const char** err) {
+  const int64_t h_out = (h - h_f) / stride + 1;
+  const int64_t w_out = (w - w_f) / stride + 1;
+  const int64_t w_eff = (w_out - 1) * stride + w_f;
+  const int64_t g_total = n * h_out;
+  const int64_t col_blocks = (w_eff + 31) / 32, c_blocks = (c + 31) / 32;
+  const int64_t total = g_total * h_f * col_blocks * c_blocks;
+  if (total >= (1ll << 32) || g_total * w_eff * h_f * c >= (1ll << 40)) {
+    *err = "im2win_transform_cl: extents exceed the kernel's index range";
+    return 1;
+  }
+  const uint32_t grid = static_cast<uint32_t>(total < 148 * 64 ? total : 148 * 64);
+  if (bf16)
+    im2win::tc::transform_cl_kernel<true><<<grid, 256, 0, stream>>>(
+        src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(h), static_cast<uint32_t>(w),
+        static_cast<uint32_t>(h_out), h_f, stride, static_cast<uint32_t>(w_eff), static_cast<uint32_t>(col_blocks),
+        static_cast<uint32_t>(c_blocks), static_cast<uint32_t>(total));
+  else
+    im2win::tc::transform_cl_kernel<false><<<grid, 256, 0, stream>>>(
+        src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(h), static_cast<uint32_t>(w),
+        static_cast<uint32_t>(h_out), h_f, stride, static_cast<uint32_t>(w_eff), static_cast<uint32_t>(col_blocks),
+        static_cast<uint32_t>(c_blocks), static_cast<uint32_t>(total));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 2;
+  }
+  return 0;
+}
+
+size_t im2win_tc_cl_workspace_bytes(int64_t c_out, int64_t K) {
+  const int64_t Mp = (c_out + 255) / 256 * 256 + 256;
+  const int64_t Kp = (K + 63) / 64 * 64;
+  return static_cast<size_t>(Mp * Kp) * 4 + 1024;
+}
+
+int im2win_launch_conv_tc_cl(const void* win_cl, const float* flt, float* out, void* workspace, int64_t n,
+                             int64_t c_in, int64_t c_out, int64_t h_out, int64_t w_out, int h_f, int w_f, int stride,
+                             int bf16, cudaStream_t stream, const char** err) {
+  using namespace im2win::tc;
+  const int64_t esz = bf16 ? 2 : 4;
+  if ((c_in * esz) % 16 != 0) {
+    *err = "im2win_conv_cl: c_in * element size must be a multiple of 16 bytes";
+    return 1;
+  }
+  const int64_t K = c_in * h_f * w_f;
+  const int64_t w_eff = (w_out - 1) * stride + w_f;
+  const int N = pick_n_cl(c_out);
+  const int bk = bf16 ? 64 : 32;
+  const int64_t Kp = (K + bk - 1) / bk * bk;
+  const int64_t Mp = (c_out + N - 1) / N * N;
+  ClArgs a{};
+  a.out = out;
+  a.g_total = static_cast<uint32_t>(n * h_out);
+  a.h_out = static_cast<uint32_t>(h_out);
+  a.w_out = static_cast<uint32_t>(w_out);
+  a.hw = static_cast<uint32_t>(h_out * w_out);
+  a.co = static_cast<uint32_t>(c_out);
+  if (w_out <= kTileM) {
+    a.box_w = static_cast<uint32_t>(w_out);
+    a.box_g = static_cast<uint32_t>(kTileM / w_out);
+  } else {
+    const int64_t parts = (w_out + kTileM - 1) / kTileM;
+    a.box_w = static_cast<uint32_t>((w_out + parts - 1) / parts);
+    a.box_g = 1;
+  }
+  if (a.box_g > 256) a.box_g = 256;
+  a.ow_tiles = (a.w_out + a.box_w - 1) / a.box_w;
+  a.g_tiles = (a.g_total + a.box_g - 1) / a.box_g;
+  if (bf16)
+    pack_filter_cl_kernel<true><<<256, 256, 0, stream>>>(flt, workspace, static_cast<int>(c_out), static_cast<int>(c_in),
+                                                         h_f, w_f, static_cast<int>(Mp), static_cast<int>(Kp));
+  else
+    pack_filter_cl_kernel<false><<<256, 256, 0, stream>>>(flt, workspace, static_cast<int>(c_out), static_cast<int>(c_in),
+                                                          h_f, w_f, static_cast<int>(Mp), static_cast<int>(Kp));
+#define IM2WIN_CL(BF, NN, ST) \
+  return launch_cl<BF, NN, ST>(a, win_cl, workspace, K, Kp, Mp, c_in, h_f, stride, w_eff, stream, err)
+  if (bf16) {
+    switch (N) {
+      case 64: IM2WIN_CL(true, 64, 8);
+      case 96: IM2WIN_CL(true, 96, 6);
+      case 128: IM2WIN_CL(true, 128, 6);
+      default: IM2WIN_CL(true, 256, 4);
+    }
+  } else {
+    switch (N) {
+      case 64: IM2WIN_CL(false, 64, 8);
+      case 96: IM2WIN_CL(false, 96, 6);
+      case 128: IM2WIN_CL(false, 128, 6);
+      default: IM2WIN_CL(false, 256, 4);
+    }
+  }
+#undef IM2WIN_CL
+}

@@ -18,7 +18,7 @@ from . import _lib
 from .errors import ShapeError
 from .layouts import Im2winTensor, im2win
 from .plan import GemmDims, TilePlan, to_c_plan
-from .tensors import DTYPE, ConvParams, Tensor4, check_conv_operands
+from .tensors import DTYPE, ConvParams, Tensor4, check_conv_operands, output_dims
 
 _workspaces: dict[tuple, torch.Tensor] = {}
 
@@ -85,10 +85,66 @@ def compute_from_windows_opt(windows: Im2winTensor, flt, params: ConvParams,
     return Tensor4(out)
 
 
+def cl_supported(c_in: int, variant: str) -> bool:
+    """The channels-innermost TMA path needs c_in * element size to be a multiple of 16 bytes."""
+    if variant == "tf32":
+        return c_in % 4 == 0
+    if variant == "bf16":
+        return c_in % 8 == 0
+    return False
+
+
+def im2win_cl_shape(inp_dims: tuple[int, int, int, int], params: ConvParams) -> tuple[int, int, int, int]:
+    """Shape of the channels-innermost window tensor: (N*Ho, w_eff, Hf, C)."""
+    n_img, c_in, h_in, w_in = inp_dims
+    h_out, w_out = output_dims(h_in, w_in, params)
+    return (n_img * h_out, (w_out - 1) * params.stride + params.w_f, params.h_f, c_in)
+
+
+def im2win_cl_into(src: torch.Tensor, dst: torch.Tensor, params: ConvParams) -> None:
+    """Channels-innermost window transform (TC fast path); dst float32 or bfloat16."""
+    n_img, c_in, h_in, w_in = (int(d) for d in src.shape)
+    dtype = 1 if dst.dtype == torch.bfloat16 else 0
+    with torch.cuda.device(src.device):
+        rc = _lib.load().im2win_transform_cl(
+            src.data_ptr(), dst.data_ptr(), n_img, c_in, h_in, w_in, params.h_f, params.w_f, params.stride, dtype,
+            torch.cuda.current_stream(src.device).cuda_stream)
+    _lib.check(rc)
+
+
+def conv_cl_into(win_cl: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, params: ConvParams,
+                 variant: str) -> None:
+    """tcgen05 convolution over the channels-innermost window tensor (TMA-fed)."""
+    n_img, c_out, h_out, w_out = (int(d) for d in out.shape)
+    code = _variant_code(variant)
+    lib = _lib.load()
+    nbytes = lib.im2win_conv_cl_workspace_bytes(params.c_in, params.c_out, params.h_f, params.w_f)
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    ws = _workspace(out.device, stream, nbytes)
+    with torch.cuda.device(out.device):
+        rc = lib.im2win_conv_cl(win_cl.data_ptr(), flt.data_ptr(), out.data_ptr(), n_img, params.c_in, c_out,
+                                h_out, w_out, params.h_f, params.w_f, params.stride, code, ws.data_ptr(),
+                                ws.numel(), stream)
+    _lib.check(rc)
+
+
 def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, *,
                     variant: str = "fp32-exact") -> Tensor4:
-    """Window-order transform followed by the tiled kernel (optimized.py:237-241)."""
+    """Window-order transform followed by the tiled kernel (optimized.py:237-241).
+
+    For the tensor-core variants with c_in*esize % 16 == 0 the transform emits the
+    channels-innermost window layout and the conv streams it with TMA (no gather);
+    otherwise (and for FP32) the reference window layout is used.
+    """
     i = inp if isinstance(inp, Tensor4) else Tensor4(inp)
     f = flt if isinstance(flt, Tensor4) else Tensor4(flt)
-    check_conv_operands(i, f, params)
+    h_out, w_out = check_conv_operands(i, f, params)
+    if cl_supported(params.c_in, variant):
+        dt = torch.bfloat16 if variant == "bf16" else torch.float32
+        win_cl = torch.empty(im2win_cl_shape(i.dims, params), dtype=dt, device=i.device)
+        im2win_cl_into(i.data, win_cl, params)
+        out = torch.empty((i.dims[0], params.c_out, h_out, w_out), dtype=DTYPE, device=i.device)
+        fd = f.data if f.device == i.device else f.data.to(i.device)
+        conv_cl_into(win_cl, fd, out, params, variant)
+        return Tensor4(out)
     return compute_from_windows_opt(im2win(i, params), f, params, plan, variant=variant)
