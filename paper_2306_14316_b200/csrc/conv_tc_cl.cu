@@ -26,41 +26,59 @@ namespace im2win {
 namespace tc {
 
 // ---------------------------------------------------------------- transform
-// CTA = (g, fh, 32 columns, 32 channels); smem transpose (c <-> col).
-template <bool BF16>
+// Work unit = (output row g, filter row fh, 32-channel block): the 32 input rows
+// X[img][c0..c0+31][oh*s+fh][0..w_eff) are staged in smem (16-byte loads when the
+// row pitch allows), then written transposed as Ĩcl[g][col][fh][c0..c0+31] with
+// 16-byte (fp32) / 8-byte (bf16) stores.  Smem pitch = 1 mod 32 makes the
+// column-wise reads conflict free.  Requires c_in % 4 == 0.
+template <bool BF16, bool VEC_IN>
 __global__ void __launch_bounds__(256) transform_cl_kernel(const float* __restrict__ src, void* __restrict__ dst,
                                                            uint32_t c_in, uint32_t h_in, uint32_t w_in,
                                                            uint32_t h_out, uint32_t h_f, uint32_t stride,
-                                                           uint32_t w_eff, uint32_t col_blocks, uint32_t c_blocks,
-                                                           uint32_t total_blocks) {
-  __shared__ float tile[32][33];
-  const uint32_t tx = threadIdx.x % 32, ty = threadIdx.x / 32;
-  for (uint32_t b = blockIdx.x; b < total_blocks; b += gridDim.x) {
-    uint32_t rest = b;
-    const uint32_t cb = rest % c_blocks;
-    rest /= c_blocks;
-    const uint32_t colb = rest % col_blocks;
-    rest /= col_blocks;
-    const uint32_t fh = rest % h_f;
-    const uint32_t g = rest / h_f;
+                                                           uint32_t w_eff, uint32_t c_blocks, uint32_t pitch,
+                                                           uint32_t total_units) {
+  extern __shared__ float tile[];  // [32][pitch]
+  const uint32_t w4 = (w_eff + 3) / 4;
+  for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x) {
+    const uint32_t cb = u % c_blocks;
+    const uint32_t fh = (u / c_blocks) % h_f;
+    const uint32_t g = u / (c_blocks * h_f);
     const uint32_t img = g / h_out, oh = g % h_out;
-    const uint32_t col0 = colb * 32, c0 = cb * 32;
-    const uint32_t row = oh * stride + fh;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t c = c0 + ty + 8 * j, col = col0 + tx;
-      float v = 0.0f;
-      if (c < c_in && col < w_eff) v = __ldg(src + ((static_cast<uint64_t>(img) * c_in + c) * h_in + row) * w_in + col);
-      tile[ty + 8 * j][tx] = v;
+    const uint32_t c0 = cb * 32;
+    const uint32_t nc = min(32u, c_in - c0);
+    const float* base = src + ((static_cast<uint64_t>(img) * c_in + c0) * h_in + oh * stride + fh) * w_in;
+    const uint64_t chan_stride = static_cast<uint64_t>(h_in) * w_in;
+    if constexpr (VEC_IN) {
+      // w_in % 4 == 0: every row is 16-byte aligned; w_eff rounded up stays inside the row
+      for (uint32_t i = threadIdx.x; i < nc * w4; i += blockDim.x) {
+        const uint32_t c = i / w4, q = i % w4;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(base + c * chan_stride) + q);
+        float* t = tile + c * pitch + q * 4;
+        t[0] = v.x; t[1] = v.y; t[2] = v.z; t[3] = v.w;
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < nc * w_eff; i += blockDim.x) {
+        const uint32_t c = i / w_eff, col = i % w_eff;
+        tile[c * pitch + col] = __ldg(base + c * chan_stride + col);
+      }
     }
     __syncthreads();
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t col = col0 + ty + 8 * j, c = c0 + tx;
-      if (c < c_in && col < w_eff) {
-        const uint64_t o = ((static_cast<uint64_t>(g) * w_eff + col) * h_f + fh) * c_in + c;
-        if constexpr (BF16) reinterpret_cast<__nv_bfloat16*>(dst)[o] = __float2bfloat16_rn(tile[tx][ty + 8 * j]);
-        else reinterpret_cast<float*>(dst)[o] = tile[tx][ty + 8 * j];
+    // thread -> (column, channel quad); 8 quads = 32 channels = one 128 B (fp32) segment
+    const uint32_t nq = nc / 4;
+    for (uint32_t i = threadIdx.x; i < w_eff * 8; i += blockDim.x) {
+      const uint32_t col = i / 8, cq = i % 8;
+      if (cq < nq) {
+        const float* t = tile + cq * 4 * pitch + col;
+        const float v0 = t[0], v1 = t[pitch], v2 = t[2 * pitch], v3 = t[3 * pitch];
+        const uint64_t o = ((static_cast<uint64_t>(g) * w_eff + col) * h_f + fh) * c_in + c0 + cq * 4;
+        if constexpr (BF16) {
+          uint2 p;
+          p.x = pack_bf16x2(v0, v1);
+          p.y = pack_bf16x2(v2, v3);
+          *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(dst) + o) = p;
+        } else {
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + o) = make_float4(v0, v1, v2, v3);
+        }
       }
     }
     __syncthreads();
@@ -314,23 +332,36 @@ int im2win_launch_transform_cl(const float* src, void* dst, int64_t n, int64_t c
   const int64_t w_out = (w - w_f) / stride + 1;
   const int64_t w_eff = (w_out - 1) * stride + w_f;
   const int64_t g_total = n * h_out;
-  const int64_t col_blocks = (w_eff + 31) / 32, c_blocks = (c + 31) / 32;
-  const int64_t total = g_total * h_f * col_blocks * c_blocks;
-  if (total >= (1ll << 32) || g_total * w_eff * h_f * c >= (1ll << 40)) {
+  const int64_t c_blocks = (c + 31) / 32;
+  const int64_t total = g_total * h_f * c_blocks;
+  if (c % 4 != 0) {
+    *err = "im2win_transform_cl: c must be a multiple of 4";
+    return 1;
+  }
+  if (total >= (1ll << 32) || n * c * h * w >= (1ll << 40)) {
     *err = "im2win_transform_cl: extents exceed the kernel's index range";
     return 1;
   }
-  const uint32_t grid = static_cast<uint32_t>(total < 148 * 64 ? total : 148 * 64);
-  if (bf16)
-    im2win::tc::transform_cl_kernel<true><<<grid, 256, 0, stream>>>(
-        src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(h), static_cast<uint32_t>(w),
-        static_cast<uint32_t>(h_out), h_f, stride, static_cast<uint32_t>(w_eff), static_cast<uint32_t>(col_blocks),
-        static_cast<uint32_t>(c_blocks), static_cast<uint32_t>(total));
-  else
-    im2win::tc::transform_cl_kernel<false><<<grid, 256, 0, stream>>>(
-        src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(h), static_cast<uint32_t>(w),
-        static_cast<uint32_t>(h_out), h_f, stride, static_cast<uint32_t>(w_eff), static_cast<uint32_t>(col_blocks),
-        static_cast<uint32_t>(c_blocks), static_cast<uint32_t>(total));
+  const uint32_t w4 = static_cast<uint32_t>((w_eff + 3) / 4);
+  const uint32_t pitch = (w4 * 4 + 31) / 32 * 32 + 1;
+  const size_t smem = static_cast<size_t>(32) * pitch * 4;
+  const uint32_t grid = static_cast<uint32_t>(total < 148 * 8 ? total : 148 * 8);
+  const bool vec = (w % 4 == 0) && (reinterpret_cast<uintptr_t>(src) % 16 == 0);
+#define IM2WIN_TCL(BF, V)                                                                                         \
+  {                                                                                                               \
+    auto k = im2win::tc::transform_cl_kernel<BF, V>;                                                              \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)); \
+    k<<<grid, 256, smem, stream>>>(src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(h),                  \
+                                   static_cast<uint32_t>(w), static_cast<uint32_t>(h_out), h_f, stride,           \
+                                   static_cast<uint32_t>(w_eff), static_cast<uint32_t>(c_blocks), pitch,          \
+                                   static_cast<uint32_t>(total));                                                 \
+  }
+  if (bf16) {
+    if (vec) IM2WIN_TCL(true, true) else IM2WIN_TCL(true, false)
+  } else {
+    if (vec) IM2WIN_TCL(false, true) else IM2WIN_TCL(false, false)
+  }
+#undef IM2WIN_TCL
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
