@@ -85,6 +85,64 @@ __global__ void __launch_bounds__(256) transform_cl_kernel(const float* __restri
   }
 }
 
+// Narrow layers: work unit = (image, block of R output rows, 32-channel block).  The
+// input rows those output rows read (span = (R-1)*s + Hf) are staged once per channel
+// and every (output row, column, filter row) of the block is written from smem, so an
+// input row is read from HBM/L2 once per unit instead of once per (g, fh).
+template <bool BF16>
+__global__ void __launch_bounds__(256) transform_cl_rows_kernel(const float* __restrict__ src, void* __restrict__ dst,
+                                                                uint32_t c_in, uint32_t h_in, uint32_t w_in,
+                                                                uint32_t h_out, uint32_t h_f, uint32_t stride,
+                                                                uint32_t w_eff, uint32_t c_blocks, uint32_t rows,
+                                                                uint32_t row_blocks, uint32_t cs,
+                                                                uint32_t total_units) {
+  extern __shared__ float tile[];  // [32][cs], row r at r*w_eff
+  for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x) {
+    const uint32_t cb = u % c_blocks;
+    const uint32_t rb = (u / c_blocks) % row_blocks;
+    const uint32_t img = u / (c_blocks * row_blocks);
+    const uint32_t oh0 = rb * rows;
+    const uint32_t nr = min(rows, h_out - oh0);
+    const uint32_t span = (nr - 1) * stride + h_f;
+    const uint32_t c0 = cb * 32;
+    const uint32_t nc = min(32u, c_in - c0);
+    const float* base = src + ((static_cast<uint64_t>(img) * c_in + c0) * h_in + oh0 * stride) * w_in;
+    const uint64_t chan_stride = static_cast<uint64_t>(h_in) * w_in;
+    const uint32_t per_c = span * w_eff;
+    for (uint32_t i = threadIdx.x; i < nc * per_c; i += blockDim.x) {
+      const uint32_t c = i / per_c, rem = i % per_c;
+      const uint32_t r = rem / w_eff, col = rem % w_eff;
+      tile[c * cs + rem] = __ldg(base + c * chan_stride + r * w_in + col);
+    }
+    __syncthreads();
+    const uint32_t nq = nc / 4;
+    const uint32_t items = nr * w_eff * h_f * 8;
+    for (uint32_t i = threadIdx.x; i < items; i += blockDim.x) {
+      const uint32_t cq = i % 8;
+      uint32_t rest = i / 8;
+      const uint32_t fh = rest % h_f;
+      rest /= h_f;
+      const uint32_t col = rest % w_eff;
+      const uint32_t ol = rest / w_eff;
+      if (cq < nq) {
+        const float* t = tile + cq * 4 * cs + (ol * stride + fh) * w_eff + col;
+        const float v0 = t[0], v1 = t[cs], v2 = t[2 * cs], v3 = t[3 * cs];
+        const uint64_t g = static_cast<uint64_t>(img) * h_out + oh0 + ol;
+        const uint64_t o = ((g * w_eff + col) * h_f + fh) * c_in + c0 + cq * 4;
+        if constexpr (BF16) {
+          uint2 p;
+          p.x = pack_bf16x2(v0, v1);
+          p.y = pack_bf16x2(v2, v3);
+          *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(dst) + o) = p;
+        } else {
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + o) = make_float4(v0, v1, v2, v3);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- GEMM
 struct ClArgs {
   float* __restrict__ out;  // (N, Co, Ho, Wo)
@@ -341,6 +399,40 @@ int im2win_launch_transform_cl(const float* src, void* dst, int64_t n, int64_t c
   if (total >= (1ll << 32) || n * c * h * w >= (1ll << 40)) {
     *err = "im2win_transform_cl: extents exceed the kernel's index range";
     return 1;
+  }
+  {
+    // narrow rows: stage whole row blocks if 32 channels x span rows x w_eff fit in 48 KB
+    const int64_t cap = 48 * 1024 / 4 / 32;  // floats per channel
+    int64_t rows = 0;
+    for (int64_t r = 1; r <= h_out; ++r) {
+      const int64_t per_c = ((r - 1) * stride + h_f) * w_eff;
+      if (per_c + 1 > cap || r * w_eff * h_f * 32 > 32 * 1024) break;
+      rows = r;
+    }
+    if (rows >= 2 || (rows == 1 && w_eff < 64)) {
+      const int64_t span = (rows - 1) * stride + h_f;
+      const uint32_t cs = static_cast<uint32_t>((span * w_eff + 31) / 32 * 32 + 1);
+      const int64_t row_blocks = (h_out + rows - 1) / rows;
+      const int64_t units = n * row_blocks * c_blocks;
+      const size_t smem = static_cast<size_t>(32) * cs * 4;
+      const uint32_t grid = static_cast<uint32_t>(units < 148 * 8 ? units : 148 * 8);
+      if (bf16)
+        im2win::tc::transform_cl_rows_kernel<true><<<grid, 256, smem, stream>>>(
+            src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(h), static_cast<uint32_t>(w),
+            static_cast<uint32_t>(h_out), h_f, stride, static_cast<uint32_t>(w_eff), static_cast<uint32_t>(c_blocks),
+            static_cast<uint32_t>(rows), static_cast<uint32_t>(row_blocks), cs, static_cast<uint32_t>(units));
+      else
+        im2win::tc::transform_cl_rows_kernel<false><<<grid, 256, smem, stream>>>(
+            src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(h), static_cast<uint32_t>(w),
+            static_cast<uint32_t>(h_out), h_f, stride, static_cast<uint32_t>(w_eff), static_cast<uint32_t>(c_blocks),
+            static_cast<uint32_t>(rows), static_cast<uint32_t>(row_blocks), cs, static_cast<uint32_t>(units));
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        *err = cudaGetErrorString(e);
+        return 2;
+      }
+      return 0;
+    }
   }
   const uint32_t w4 = static_cast<uint32_t>((w_eff + 3) / 4);
   const uint32_t pitch = (w4 * 4 + 31) / 32 * 32 + 1;
