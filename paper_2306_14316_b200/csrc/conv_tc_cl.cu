@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(256) transform_cl_rows_kernel(const float* __r
                                                                 uint32_t h_out, uint32_t h_f, uint32_t stride,
                                                                 uint32_t w_eff, uint32_t c_blocks, uint32_t rows,
                                                                 uint32_t row_blocks, uint32_t cs,
-                                                                uint32_t total_units) {
+                                                                uint32_t total_units, FastDiv fd_weff, FastDiv fd_hf) {
   extern __shared__ float tile[];  // [32][cs], row r at r*w_eff
   for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x) {
     const uint32_t cb = u % c_blocks;
@@ -109,21 +109,21 @@ __global__ void __launch_bounds__(256) transform_cl_rows_kernel(const float* __r
     const float* base = src + ((static_cast<uint64_t>(img) * c_in + c0) * h_in + oh0 * stride) * w_in;
     const uint64_t chan_stride = static_cast<uint64_t>(h_in) * w_in;
     const uint32_t per_c = span * w_eff;
+    const FastDiv fd_perc(per_c);
     for (uint32_t i = threadIdx.x; i < nc * per_c; i += blockDim.x) {
-      const uint32_t c = i / per_c, rem = i % per_c;
-      const uint32_t r = rem / w_eff, col = rem % w_eff;
+      uint32_t c, rem, r, col;
+      fd_perc.divmod(i, c, rem);
+      fd_weff.divmod(rem, r, col);
       tile[c * cs + rem] = __ldg(base + c * chan_stride + r * w_in + col);
     }
     __syncthreads();
     const uint32_t nq = nc / 4;
     const uint32_t items = nr * w_eff * h_f * 8;
     for (uint32_t i = threadIdx.x; i < items; i += blockDim.x) {
-      const uint32_t cq = i % 8;
-      uint32_t rest = i / 8;
-      const uint32_t fh = rest % h_f;
-      rest /= h_f;
-      const uint32_t col = rest % w_eff;
-      const uint32_t ol = rest / w_eff;
+      const uint32_t cq = i & 7;
+      uint32_t rest, fh, col, ol;
+      fd_hf.divmod(i >> 3, rest, fh);
+      fd_weff.divmod(rest, ol, col);
       if (cq < nq) {
         const float* t = tile + cq * 4 * cs + (ol * stride + fh) * w_eff + col;
         const float v0 = t[0], v1 = t[cs], v2 = t[2 * cs], v3 = t[3 * cs];
@@ -406,7 +406,7 @@ int im2win_launch_transform_cl(const float* src, void* dst, int64_t n, int64_t c
     int64_t rows = 0;
     for (int64_t r = 1; r <= h_out; ++r) {
       const int64_t per_c = ((r - 1) * stride + h_f) * w_eff;
-      if (per_c + 1 > cap || r * w_eff * h_f * 32 > 32 * 1024) break;
+      if ((per_c + 31) / 32 * 32 + 1 > cap || r * w_eff * h_f * 32 > 32 * 1024) break;
       rows = r;
     }
     if (rows >= 2 || (rows == 1 && w_eff < 64)) {
@@ -420,12 +420,14 @@ int im2win_launch_transform_cl(const float* src, void* dst, int64_t n, int64_t c
         im2win::tc::transform_cl_rows_kernel<true><<<grid, 256, smem, stream>>>(
             src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(h), static_cast<uint32_t>(w),
             static_cast<uint32_t>(h_out), h_f, stride, static_cast<uint32_t>(w_eff), static_cast<uint32_t>(c_blocks),
-            static_cast<uint32_t>(rows), static_cast<uint32_t>(row_blocks), cs, static_cast<uint32_t>(units));
+            static_cast<uint32_t>(rows), static_cast<uint32_t>(row_blocks), cs, static_cast<uint32_t>(units),
+            im2win::FastDiv(static_cast<uint32_t>(w_eff)), im2win::FastDiv(static_cast<uint32_t>(h_f)));
       else
         im2win::tc::transform_cl_rows_kernel<false><<<grid, 256, smem, stream>>>(
             src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(h), static_cast<uint32_t>(w),
             static_cast<uint32_t>(h_out), h_f, stride, static_cast<uint32_t>(w_eff), static_cast<uint32_t>(c_blocks),
-            static_cast<uint32_t>(rows), static_cast<uint32_t>(row_blocks), cs, static_cast<uint32_t>(units));
+            static_cast<uint32_t>(rows), static_cast<uint32_t>(row_blocks), cs, static_cast<uint32_t>(units),
+            im2win::FastDiv(static_cast<uint32_t>(w_eff)), im2win::FastDiv(static_cast<uint32_t>(h_f)));
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) {
         *err = cudaGetErrorString(e);
