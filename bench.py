@@ -160,6 +160,7 @@ def main() -> None:
     ap.add_argument("--layers", default="all")
     ap.add_argument("--no-baselines", action="store_true", help="skip cuDNN / im2col+cuBLAS / CPU legs")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-tc", action="store_true", help="skip the TF32/BF16 tensor-core section")
     args = ap.parse_args()
 
     if args.impl == "reference":
@@ -405,6 +406,70 @@ def main() -> None:
         cpu_baseline = {"value": sum(c.flops for c in cfgs) / dt / 1e12, "unit": "TFLOPS", "cores": threads,
                         "kind": "port", "sample": f"12 layers at N=1 image, {reps} reps (per-image slice of the workload)"}
 
+    # ---- tensor-core variants (rank 0): TF32 / BF16 per layer at N=128 and config 4 ----
+    tc = None
+    if rank == 0 and not args.no_tc:
+        from paper_2306_14316_b200.kernels import cl_supported, conv_cl_into, im2win_cl_into, im2win_cl_shape
+
+        def tc_layer(cfg, v):
+            """transform + conv time (ms) of the production TC path for one layer."""
+            h_out, w_out = cfg.out_dims
+            g2 = torch.Generator(device=dev).manual_seed(cfg.seed)
+            x = torch.randn((cfg.batch, cfg.c_in, cfg.h_in, cfg.w_in), device=dev, generator=g2)
+            f = torch.randn((cfg.c_out, cfg.c_in, cfg.h_f, cfg.w_f), device=dev, generator=g2)
+            o = torch.empty((cfg.batch, cfg.c_out, h_out, w_out), device=dev)
+            if cl_supported(cfg.c_in, v):
+                w = torch.empty(im2win_cl_shape((cfg.batch, cfg.c_in, cfg.h_in, cfg.w_in), cfg.params),
+                                dtype=torch.bfloat16 if v == "bf16" else torch.float32, device=dev)
+                tr = lambda: im2win_cl_into(x, w, cfg.params)  # noqa: E731
+                cv = lambda: conv_cl_into(w, f, o, cfg.params, v)  # noqa: E731
+                path = "im2win-cl + TMA tcgen05"
+            else:
+                w = torch.empty((cfg.batch, cfg.c_in, h_out, cfg.h_f * cfg.w_eff), device=dev)
+                tr = lambda: im2win_into(x, w, cfg.params)  # noqa: E731
+                cv = lambda: conv_windows_into(w, f, o, cfg.params, cfg.w_eff, None, v)  # noqa: E731
+                path = "im2win + gathered tcgen05"
+            tr()
+            cv()
+            best_t = best_c = 1e30
+            for _ in range(3):
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                e[0].record(stream)
+                tr()
+                e[1].record(stream)
+                cv()
+                e[2].record(stream)
+                torch.cuda.synchronize(dev)
+                best_t = min(best_t, e[0].elapsed_time(e[1]))
+                best_c = min(best_c, e[1].elapsed_time(e[2]))
+            del x, f, o, w
+            torch.cuda.empty_cache()
+            return best_t, best_c, path
+
+        tc = {"tolerance": {"tf32": "max|d|/rms(ref) <= 1e-2", "bf16": "max|d|/rms(ref) <= 4e-2"},
+              "peak_tensor_tflops": {"bf16": peaks.get("bf16_tflops"), "tf32": None,
+                                     "source": peaks["source"] + " (tf32: no measured peak; nominal 1100)"}}
+        for v in ("tf32", "bf16"):
+            rows = {}
+            tot_f = tot_ms = 0.0
+            for L in layers:
+                cfg = L["cfg"]
+                t_tr, t_cv, path = tc_layer(cfg, v)
+                rows[cfg.name] = {"tflops": cfg.flops / ((t_tr + t_cv) * 1e-3) / 1e12,
+                                  "tflops_conv_only": cfg.flops / (t_cv * 1e-3) / 1e12,
+                                  "transform_ms": t_tr, "conv_ms": t_cv, "path": path}
+                tot_f += cfg.flops
+                tot_ms += t_tr + t_cv
+            tc[v] = {"layers_n128": rows, "step_tflops_n128": tot_f / (tot_ms * 1e-3) / 1e12}
+            # config 4: ResNet-50 3x3 layers (conv9-12) at N=1024 per GPU
+            c4 = {}
+            for name in ("conv9", "conv10", "conv11", "conv12"):
+                cfg = replace(BENCHMARKS[name], batch=1024, seed=4000)
+                t_tr, t_cv, path = tc_layer(cfg, v)
+                c4[name] = {"tflops": cfg.flops / ((t_tr + t_cv) * 1e-3) / 1e12,
+                            "tflops_conv_only": cfg.flops / (t_cv * 1e-3) / 1e12, "path": path}
+            tc[v]["config4_n1024"] = c4
+
     n_layers = len(layers)
     line = {
         "metric": "TFLOPS per conv layer (12 benchmarks) at 1/2/4/8 B200; memory footprint",
@@ -424,6 +489,7 @@ def main() -> None:
         "clocks": clocks,
         "layers": per_layer,
         "baselines": baselines,
+        "tensor_core_variants": tc,
         "peaks": {"fp32_exact_tflops": peak["exact"], "fp32_ffma_tflops": peak["ffma"],
                   "hbm_gbs": peaks["hbm_gbs"], "source": peaks["source"]},
     }
