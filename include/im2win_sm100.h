@@ -93,6 +93,19 @@ int im2win_conv_cl(const void* windows_cl, const float* flt, float* out, int64_t
                    int32_t stride, int32_t variant, void* workspace, size_t workspace_bytes,
                    void* stream);
 
+/* ---- Fused tensor-core path (extension): no materialised window tensor ----
+ * im2win_nchw_to_nhwc copies X to channels-last (dtype 0 f32, 1 bf16; c % 4 == 0);
+ * im2win_conv_fused then reads every window row Xnhwc[n][oh*s+fh][ow*s..ow*s+w_f-1][:]
+ * with one 5-D TMA box per K-slab (the windows are built by the TMA engine). */
+int im2win_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w,
+                        int32_t dtype, void* stream);
+
+size_t im2win_conv_fused_workspace_bytes(int64_t c_in, int64_t c_out, int32_t h_f, int32_t w_f);
+
+int im2win_conv_fused(const void* x_nhwc, const float* flt, float* out, int64_t n, int64_t c_in,
+                      int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
+                      int32_t variant, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Measurement utility (bench.py only): launches `blocks` x 256 threads that each
  * retire 2*32*iters flops of independent FP32 multiply-add chains; exact != 0
  * issues FMUL+FADD (the conv's bit-exact pair), else FFMA.  Used to measure the

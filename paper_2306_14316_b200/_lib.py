@@ -33,6 +33,9 @@ EXPORTED_SYMBOLS = (
     "im2win_transform_cl",
     "im2win_conv_cl_workspace_bytes",
     "im2win_conv_cl",
+    "im2win_nchw_to_nhwc",
+    "im2win_conv_fused_workspace_bytes",
+    "im2win_conv_fused",
 )
 
 
@@ -82,6 +85,12 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         lib.im2win_conv_cl_workspace_bytes.restype = sz
         lib.im2win_conv_cl.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32, i32, vp, sz, vp]
         lib.im2win_conv_cl.restype = ctypes.c_int
+        lib.im2win_nchw_to_nhwc.argtypes = [vp, vp, i64, i64, i64, i64, i32, vp]
+        lib.im2win_nchw_to_nhwc.restype = ctypes.c_int
+        lib.im2win_conv_fused_workspace_bytes.argtypes = [i64, i64, i32, i32]
+        lib.im2win_conv_fused_workspace_bytes.restype = sz
+        lib.im2win_conv_fused.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32, i32, vp, sz, vp]
+        lib.im2win_conv_fused.restype = ctypes.c_int
         if path is None:
             _lib = lib
         return lib

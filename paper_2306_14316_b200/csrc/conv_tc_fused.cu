@@ -1,0 +1,401 @@
+// Fused ("implicit") im2win tensor-core convolution: window tiles are built by TMA
+// straight from a channels-last copy of the input, so Ĩ is never materialised.
+//
+// With Xcl[n][h][w][c] (NHWC), the im2win window row of filter row fh for output pixel
+// (n, oh, ow) is ONE contiguous run of Wf*C elements, Xcl[n][oh*s+fh][ow*s .. ow*s+Wf-1][:],
+// i.e. exactly the channels-last window row of the im2win layout (layouts.py:73-83 stores
+// the same Hf rows per output row; here the TMA engine gathers them per tile).  The GEMM
+// operand is therefore the strided 5-D view
+//     A[(n, oh, ow)][(fh, j)] = Xcl + n*H*W*C + (oh*s + fh)*W*C + ow*s*C + j,  j < Wf*C
+// {j, fh, ow, oh, n} with strides {1, W*C, s*C, s*W*C, H*W*C} elements, which one
+// cp.async.bulk.tensor.5d per K-slab streams into the 128-byte-swizzled K-major smem
+// tile tcgen05.mma reads.  K-slabs run over (fh, 32/64-wide chunks of j); the pixel
+// tile is a box of box_w x box_h x box_n output pixels (<= 128 = UMMA M).
+// HBM traffic: read X, write Xcl (1x input), the conv reads Xcl (L2 absorbs the
+// Hf*Wf/s^2 window overlap) -- versus writing and re-reading the 2-4x larger Ĩ.
+#include <stddef.h>
+#include <algorithm>
+#include <stdint.h>
+
+#include "tc_common.cuh"
+
+namespace im2win {
+namespace tc {
+
+// NCHW float32 -> NHWC (float32 or bf16): per image a [C][H*W] -> [H*W][C] transpose.
+template <bool BF16>
+__global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restrict__ src, void* __restrict__ dst,
+                                                           uint32_t c_in, uint32_t hw, uint32_t hw_tiles,
+                                                           uint32_t c_tiles, uint32_t total) {
+  __shared__ float tile[32][33];
+  const uint32_t tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
+    const uint32_t ct = b % c_tiles;
+    const uint32_t pt = (b / c_tiles) % hw_tiles;
+    const uint32_t img = b / (c_tiles * hw_tiles);
+    const uint32_t c0 = ct * 32, p0 = pt * 32;
+    const float* s = src + static_cast<uint64_t>(img) * c_in * hw;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t c = c0 + ty + 8 * j, p = p0 + tx;
+      tile[ty + 8 * j][tx] = (c < c_in && p < hw) ? __ldg(s + static_cast<uint64_t>(c) * hw + p) : 0.0f;
+    }
+    __syncthreads();
+    // write: 8 threads per pixel, 4 channels each (16 B fp32 / 8 B bf16)
+    const uint32_t pl = threadIdx.x / 8, cq = threadIdx.x % 8;
+    const uint32_t p = p0 + pl, c = c0 + cq * 4;
+    if (p < hw && c < c_in) {
+      const float v0 = tile[cq * 4][pl], v1 = tile[cq * 4 + 1][pl], v2 = tile[cq * 4 + 2][pl], v3 = tile[cq * 4 + 3][pl];
+      const uint64_t o = (static_cast<uint64_t>(img) * hw + p) * c_in + c;
+      if constexpr (BF16) {
+        uint2 q;
+        q.x = pack_bf16x2(v0, v1);
+        q.y = pack_bf16x2(v2, v3);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(dst) + o) = q;
+      } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + o) = make_float4(v0, v1, v2, v3);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+struct FusedArgs {
+  float* __restrict__ out;
+  uint32_t n_img, h_out, w_out, hw, co;
+  uint32_t box_w, box_h, box_n;
+  uint32_t ow_tiles, oh_tiles, n_tiles, co_tiles;
+  uint32_t k_slabs, fh_slabs;  // k_slabs = Hf * fh_slabs
+};
+
+template <bool BF16, int N, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+    conv_tc_fused_kernel(const FusedArgs a, const __grid_constant__ CUtensorMap tmap_a,
+                         const __grid_constant__ CUtensorMap tmap_b) {
+  constexpr uint32_t kABytes = kTileM * kRowBytes;
+  constexpr uint32_t kBBytes = N * kRowBytes;
+  constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  constexpr int kBK = BF16 ? 64 : 32;
+  constexpr int kUK = BF16 ? 16 : 8;
+  constexpr uint32_t kTmemCols = (2 * N <= 128) ? 128 : (2 * N <= 256 ? 256 : 512);
+  constexpr uint32_t kIdesc = instr_desc<BF16, N>();
+
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t tfull_bar[2];
+  __shared__ __align__(8) uint64_t tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t pix_per_tile = a.box_w * a.box_h * a.box_n;
+  const uint32_t a_box_bytes = pix_per_tile * kRowBytes;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);
+    }
+    fence_barrier_init();
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap_b) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+  const uint32_t total_tiles = a.n_tiles * a.oh_tiles * a.ow_tiles * a.co_tiles;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const uint32_t co_blk = t % a.co_tiles;
+        uint32_t pt = t / a.co_tiles;
+        const uint32_t ow0 = (pt % a.ow_tiles) * a.box_w;
+        pt /= a.ow_tiles;
+        const uint32_t oh0 = (pt % a.oh_tiles) * a.box_h;
+        const uint32_t n0 = (pt / a.oh_tiles) * a.box_n;
+        for (uint32_t ks = 0; ks < a.k_slabs; ++ks) {
+          const uint32_t fh = ks / a.fh_slabs;
+          const uint32_t j0 = (ks % a.fh_slabs) * kBK;
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* st = smem + stage * kStageBytes;
+          mbar_arrive_expect_tx(&full_bar[stage], a_box_bytes + kBBytes);
+          asm volatile(
+              "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, "
+              "%7}], [%2];\n" ::"r"(smem_u32(st)),
+              "l"(&tmap_a), "r"(smem_u32(&full_bar[stage])), "r"(j0), "r"(fh), "r"(ow0), "r"(oh0), "r"(n0)
+              : "memory");
+          tma_load_2d(st + kABytes, &tmap_b, &full_bar[stage], ks * kBK, co_blk * N);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * N;
+        for (uint32_t ks = 0; ks < a.k_slabs; ++ks) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t abase = smem_u32(smem + stage * kStageBytes);
+          const uint32_t bbase = abase + kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / kUK; ++kk)
+            mma<BF16>(tmem_d, smem_desc_sw128(abase + kk * 32), smem_desc_sw128(bbase + kk * 32), kIdesc,
+                      (ks | kk) != 0);
+          mma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull_bar[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int quarter = warp % 4;
+    const uint32_t r = quarter * 32 + lane;
+    const uint32_t r_w = r % a.box_w, r_h = (r / a.box_w) % a.box_h, r_n = r / (a.box_w * a.box_h);
+    uint32_t acc = 0, acc_phase = 0;
+    for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const uint32_t co_blk = t % a.co_tiles;
+      uint32_t pt = t / a.co_tiles;
+      const uint32_t ow = (pt % a.ow_tiles) * a.box_w + r_w;
+      pt /= a.ow_tiles;
+      const uint32_t oh = (pt % a.oh_tiles) * a.box_h + r_h;
+      const uint32_t img = (pt / a.oh_tiles) * a.box_n + r_n;
+      const bool valid = r < pix_per_tile && ow < a.w_out && oh < a.h_out && img < a.n_img;
+      const int64_t obase = valid ? static_cast<int64_t>(img) * a.co * a.hw + static_cast<int64_t>(oh) * a.w_out + ow : 0;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * N;
+#pragma unroll
+      for (int j0 = 0; j0 < N; j0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(taddr + j0, v);
+        const uint32_t m0 = co_blk * N + j0;
+        if (valid) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (m0 + q < a.co) a.out[obase + static_cast<int64_t>(m0 + q) * a.hw] = __uint_as_float(v[q]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(kTmemCols));
+  }
+}
+
+// B[m][fh*Kfh + j] = F[m][c][fh][fw] for j = fw*C + c < Wf*C, zero elsewhere.
+template <bool BF16>
+__global__ void pack_filter_fused_kernel(const float* __restrict__ flt, void* __restrict__ packed, int M, int C,
+                                         int h_f, int w_f, int Mp, int Kfh, int Kp) {
+  const int64_t total = static_cast<int64_t>(Mp) * Kp;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(i / Kp);
+    const int kp = static_cast<int>(i % Kp);
+    const int fh = kp / Kfh, j = kp % Kfh;
+    float v = 0.0f;
+    if (m < M && j < w_f * C) {
+      const int fw = j / C, c = j % C;
+      v = flt[((static_cast<int64_t>(m) * C + c) * h_f + fh) * w_f + fw];
+    }
+    if constexpr (BF16) {
+      reinterpret_cast<__nv_bfloat16*>(packed)[i] = __float2bfloat16_rn(v);
+    } else {
+      uint32_t r;
+      asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(v));
+      reinterpret_cast<uint32_t*>(packed)[i] = r;
+    }
+  }
+}
+
+template <bool BF16, int N, int STAGES>
+static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64_t c_in, int64_t h, int64_t w,
+                        int32_t h_f, int32_t w_f, int32_t stride, int64_t Kp, int64_t Mp, cudaStream_t stream,
+                        const char** err) {
+  constexpr int kBK = BF16 ? 64 : 32;
+  auto enc = get_encode_fn();
+  if (!enc) {
+    *err = "conv_tc_fused: cuTensorMapEncodeTiled unavailable";
+    return 2;
+  }
+  const cuuint64_t esz = BF16 ? 2 : 4;
+  const CUtensorMapDataType dt = BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUtensorMap map_a, map_b;
+  {
+    cuuint64_t dims[5] = {static_cast<cuuint64_t>(w_f) * c_in, static_cast<cuuint64_t>(h_f), a.w_out, a.h_out,
+                          a.n_img};
+    cuuint64_t strides[4] = {static_cast<cuuint64_t>(w) * c_in * esz, static_cast<cuuint64_t>(stride) * c_in * esz,
+                             static_cast<cuuint64_t>(stride) * w * c_in * esz,
+                             static_cast<cuuint64_t>(h) * w * c_in * esz};
+    cuuint32_t box[5] = {static_cast<cuuint32_t>(kBK), 1, a.box_w, a.box_h, a.box_n};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = enc(&map_a, dt, 5, const_cast<void*>(x_cl), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      *err = "conv_tc_fused: window tensor map rejected (cuTensorMapEncodeTiled)";
+      return 2;
+    }
+  }
+  {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(Mp)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(Kp) * esz};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(N)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&map_b, dt, 2, const_cast<void*>(packed), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      *err = "conv_tc_fused: filter tensor map rejected (cuTensorMapEncodeTiled)";
+      return 2;
+    }
+  }
+  a.co_tiles = static_cast<uint32_t>(Mp / N);
+  const size_t smem = static_cast<size_t>(STAGES) * (kTileM + N) * kRowBytes + 1024;
+  auto kern = conv_tc_fused_kernel<BF16, N, STAGES>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 2;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t tiles = static_cast<uint64_t>(a.n_tiles) * a.oh_tiles * a.ow_tiles * a.co_tiles;
+  const uint32_t grid = tiles < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(tiles) : static_cast<uint32_t>(sms);
+  kern<<<grid, 256, smem, stream>>>(a, map_a, map_b);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 2;
+  }
+  return 0;
+}
+
+}  // namespace tc
+}  // namespace im2win
+
+int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w, int bf16,
+                               cudaStream_t stream, const char** err) {
+  const int64_t hw = h * w;
+  const int64_t hw_tiles = (hw + 31) / 32, c_tiles = (c + 31) / 32;
+  const int64_t total = n * hw_tiles * c_tiles;
+  if (c % 4 != 0 || total >= (1ll << 32) || hw >= (1ll << 31)) {
+    *err = "nchw_to_nhwc: c must be a multiple of 4 and extents within range";
+    return 1;
+  }
+  const uint32_t grid = static_cast<uint32_t>(total < 148 * 16 ? total : 148 * 16);
+  if (bf16)
+    im2win::tc::nchw_to_nhwc_kernel<true><<<grid, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
+                                                                     static_cast<uint32_t>(hw),
+                                                                     static_cast<uint32_t>(hw_tiles),
+                                                                     static_cast<uint32_t>(c_tiles),
+                                                                     static_cast<uint32_t>(total));
+  else
+    im2win::tc::nchw_to_nhwc_kernel<false><<<grid, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
+                                                                      static_cast<uint32_t>(hw),
+                                                                      static_cast<uint32_t>(hw_tiles),
+                                                                      static_cast<uint32_t>(c_tiles),
+                                                                      static_cast<uint32_t>(total));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 2;
+  }
+  return 0;
+}
+
+size_t im2win_tc_fused_workspace_bytes(int64_t c_in, int64_t c_out, int h_f, int w_f) {
+  const int64_t Mp = (c_out + 255) / 256 * 256 + 256;
+  const int64_t Kfh = (w_f * c_in + 63) / 64 * 64;
+  return static_cast<size_t>(Mp * Kfh * h_f) * 4 + 1024;
+}
+
+int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n,
+                                int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride,
+                                int bf16, cudaStream_t stream, const char** err) {
+  using namespace im2win::tc;
+  const int64_t esz = bf16 ? 2 : 4;
+  if ((c_in * esz) % 16 != 0) {
+    *err = "im2win_conv_fused: c_in * element size must be a multiple of 16 bytes";
+    return 1;
+  }
+  const int64_t h_out = (h - h_f) / stride + 1, w_out = (w - w_f) / stride + 1;
+  const int N = c_out <= 64 ? 64 : c_out <= 96 ? 96 : c_out <= 128 ? 128 : 256;
+  const int bk = bf16 ? 64 : 32;
+  const int64_t Kfh = (w_f * c_in + bk - 1) / bk * bk;
+  const int64_t Kp = Kfh * h_f;
+  const int64_t Mp = (c_out + N - 1) / N * N;
+  FusedArgs a{};
+  a.out = out;
+  a.n_img = static_cast<uint32_t>(n);
+  a.h_out = static_cast<uint32_t>(h_out);
+  a.w_out = static_cast<uint32_t>(w_out);
+  a.hw = static_cast<uint32_t>(h_out * w_out);
+  a.co = static_cast<uint32_t>(c_out);
+  if (w_out > kTileM) {
+    const int64_t parts = (w_out + kTileM - 1) / kTileM;
+    a.box_w = static_cast<uint32_t>((w_out + parts - 1) / parts);
+    a.box_h = 1;
+    a.box_n = 1;
+  } else {
+    a.box_w = static_cast<uint32_t>(w_out);
+    a.box_h = static_cast<uint32_t>(std::min<int64_t>(h_out, kTileM / w_out));
+    a.box_n = a.box_h == h_out ? static_cast<uint32_t>(std::min<int64_t>(n, kTileM / (w_out * h_out))) : 1u;
+  }
+  a.ow_tiles = (a.w_out + a.box_w - 1) / a.box_w;
+  a.oh_tiles = (a.h_out + a.box_h - 1) / a.box_h;
+  a.n_tiles = (a.n_img + a.box_n - 1) / a.box_n;
+  a.fh_slabs = static_cast<uint32_t>(Kfh / bk);
+  a.k_slabs = a.fh_slabs * h_f;
+  if (bf16)
+    pack_filter_fused_kernel<true><<<256, 256, 0, stream>>>(flt, workspace, static_cast<int>(c_out),
+                                                            static_cast<int>(c_in), h_f, w_f, static_cast<int>(Mp),
+                                                            static_cast<int>(Kfh), static_cast<int>(Kp));
+  else
+    pack_filter_fused_kernel<false><<<256, 256, 0, stream>>>(flt, workspace, static_cast<int>(c_out),
+                                                             static_cast<int>(c_in), h_f, w_f, static_cast<int>(Mp),
+                                                             static_cast<int>(Kfh), static_cast<int>(Kp));
+#define IM2WIN_FU(BF, NN, ST) \
+  return launch_fused<BF, NN, ST>(a, x_cl, workspace, c_in, h, w, h_f, w_f, stride, Kp, Mp, stream, err)
+  if (bf16) {
+    switch (N) {
+      case 64: IM2WIN_FU(true, 64, 8);
+      case 96: IM2WIN_FU(true, 96, 6);
+      case 128: IM2WIN_FU(true, 128, 6);
+      default: IM2WIN_FU(true, 256, 4);
+    }
+  } else {
+    switch (N) {
+      case 64: IM2WIN_FU(false, 64, 8);
+      case 96: IM2WIN_FU(false, 96, 6);
+      case 128: IM2WIN_FU(false, 128, 6);
+      default: IM2WIN_FU(false, 256, 4);
+    }
+  }
+#undef IM2WIN_FU
+}

@@ -128,18 +128,61 @@ def conv_cl_into(win_cl: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, par
     _lib.check(rc)
 
 
+def nhwc_into(src: torch.Tensor, dst: torch.Tensor) -> None:
+    """NCHW float32 -> channels-last copy (float32 or bfloat16) for the fused TC path."""
+    n_img, c_in, h_in, w_in = (int(d) for d in src.shape)
+    dtype = 1 if dst.dtype == torch.bfloat16 else 0
+    with torch.cuda.device(src.device):
+        rc = _lib.load().im2win_nchw_to_nhwc(src.data_ptr(), dst.data_ptr(), n_img, c_in, h_in, w_in, dtype,
+                                             torch.cuda.current_stream(src.device).cuda_stream)
+    _lib.check(rc)
+
+
+def conv_fused_into(x_nhwc: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, params: ConvParams,
+                    variant: str) -> None:
+    """tcgen05 convolution whose window tiles TMA builds from the channels-last input."""
+    n_img, h_in, w_in, c_in = (int(d) for d in x_nhwc.shape)
+    code = _variant_code(variant)
+    lib = _lib.load()
+    nbytes = lib.im2win_conv_fused_workspace_bytes(params.c_in, params.c_out, params.h_f, params.w_f)
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    ws = _workspace(out.device, stream, nbytes)
+    with torch.cuda.device(out.device):
+        rc = lib.im2win_conv_fused(x_nhwc.data_ptr(), flt.data_ptr(), out.data_ptr(), n_img, c_in, h_in, w_in,
+                                   params.c_out, params.h_f, params.w_f, params.stride, code, ws.data_ptr(),
+                                   ws.numel(), stream)
+    _lib.check(rc)
+
+
+TC_PATHS = ("auto", "fused", "cl", "gather")
+
+
 def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, *,
-                    variant: str = "fp32-exact") -> Tensor4:
+                    variant: str = "fp32-exact", tc_path: str = "auto") -> Tensor4:
     """Window-order transform followed by the tiled kernel (optimized.py:237-241).
 
-    For the tensor-core variants with c_in*esize % 16 == 0 the transform emits the
-    channels-innermost window layout and the conv streams it with TMA (no gather);
-    otherwise (and for FP32) the reference window layout is used.
+    FP32 variants use the reference window layout Ĩ.  Tensor-core variants pick
+    (tc_path="auto"): "fused" — TMA builds window tiles from a channels-last copy
+    of the input (no Ĩ); "cl" — materialised channels-innermost Ĩ streamed by TMA;
+    "gather" — reference Ĩ gathered by producer warps.  fused/cl need
+    c_in * element size to be a multiple of 16 bytes; otherwise gather is used.
     """
+    if tc_path not in TC_PATHS:
+        raise ValueError(f"tc_path must be one of {TC_PATHS}")
     i = inp if isinstance(inp, Tensor4) else Tensor4(inp)
     f = flt if isinstance(flt, Tensor4) else Tensor4(flt)
     h_out, w_out = check_conv_operands(i, f, params)
-    if cl_supported(params.c_in, variant):
+    ok = cl_supported(params.c_in, variant)
+    if ok and tc_path in ("auto", "fused"):
+        dt = torch.bfloat16 if variant == "bf16" else torch.float32
+        n_img, c_in, h_in, w_in = i.dims
+        x_cl = torch.empty((n_img, h_in, w_in, c_in), dtype=dt, device=i.device)
+        nhwc_into(i.data, x_cl)
+        out = torch.empty((n_img, params.c_out, h_out, w_out), dtype=DTYPE, device=i.device)
+        fd = f.data if f.device == i.device else f.data.to(i.device)
+        conv_fused_into(x_cl, fd, out, params, variant)
+        return Tensor4(out)
+    if ok and tc_path == "cl":
         dt = torch.bfloat16 if variant == "bf16" else torch.float32
         win_cl = torch.empty(im2win_cl_shape(i.dims, params), dtype=dt, device=i.device)
         im2win_cl_into(i.data, win_cl, params)
