@@ -409,7 +409,7 @@ def main() -> None:
     # ---- tensor-core variants (rank 0): TF32 / BF16 per layer at N=128 and config 4 ----
     tc = None
     if rank == 0 and not args.no_tc:
-        from paper_2306_14316_b200.kernels import cl_supported, conv_cl_into, im2win_cl_into, im2win_cl_shape
+        from paper_2306_14316_b200.kernels import cl_supported, conv_fused_into, nhwc_into
 
         def tc_layer(cfg, v):
             """transform + conv time (ms) of the production TC path for one layer."""
@@ -419,11 +419,11 @@ def main() -> None:
             f = torch.randn((cfg.c_out, cfg.c_in, cfg.h_f, cfg.w_f), device=dev, generator=g2)
             o = torch.empty((cfg.batch, cfg.c_out, h_out, w_out), device=dev)
             if cl_supported(cfg.c_in, v):
-                w = torch.empty(im2win_cl_shape((cfg.batch, cfg.c_in, cfg.h_in, cfg.w_in), cfg.params),
+                w = torch.empty((cfg.batch, cfg.h_in, cfg.w_in, cfg.c_in),
                                 dtype=torch.bfloat16 if v == "bf16" else torch.float32, device=dev)
-                tr = lambda: im2win_cl_into(x, w, cfg.params)  # noqa: E731
-                cv = lambda: conv_cl_into(w, f, o, cfg.params, v)  # noqa: E731
-                path = "im2win-cl + TMA tcgen05"
+                tr = lambda: nhwc_into(x, w)  # noqa: E731
+                cv = lambda: conv_fused_into(w, f, o, cfg.params, v)  # noqa: E731
+                path = "fused: NHWC copy + 5-D TMA window boxes -> tcgen05"
             else:
                 w = torch.empty((cfg.batch, cfg.c_in, h_out, cfg.h_f * cfg.w_eff), device=dev)
                 tr = lambda: im2win_into(x, w, cfg.params)  # noqa: E731

@@ -171,3 +171,33 @@ def test_tc_large_batch_sampled_images(variant):
     for i in (0, 77, 127):
         ref = orc.conv_direct(inp[i:i + 1].numpy(), flt.numpy(), cfg.stride)
         assert pkg.normalized_max_diff(out.data[i:i + 1].cpu().numpy(), ref) <= TC_TOL[variant]
+
+
+@pytest.mark.parametrize("tc_path", ["fused", "cl", "gather"])
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_tc_paths_all_layers(tc_path, variant, layer_goldens):
+    """Every tensor-core path (fused TMA windows / materialised channels-last Ĩ /
+    gathered reference Ĩ) stays within the stated tolerance on the 12 layers."""
+    for name in BENCHMARKS:
+        g = layer_goldens[name]
+        cfg = replace(BENCHMARKS[name], batch=g["batch"], seed=g["seed"])
+        inp, flt = make_inputs(cfg)
+        ref = orc.conv_direct(inp, flt, cfg.stride)
+        out = pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant, tc_path=tc_path).numpy()
+        assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (name, tc_path)
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_tc_fused_odd_geometries(variant):
+    """Fused path edge cases: partial pixel tiles, strides, Co not a multiple of the
+    UMMA N tile, multi-image boxes, tiny images."""
+    rng = np.random.default_rng(21)
+    cases = [(3, 16, 9, 11, 20, 3, 3, 1), (2, 32, 13, 13, 40, 5, 3, 2), (5, 64, 7, 7, 130, 3, 3, 1),
+             (1, 8, 4, 4, 3, 2, 2, 1), (4, 96, 10, 9, 257, 1, 1, 1), (2, 16, 33, 31, 17, 7, 5, 3)]
+    for (n, c, h, w, co, hf, wf, s) in cases:
+        inp = rng.standard_normal((n, c, h, w), dtype=np.float32)
+        flt = rng.standard_normal((co, c, hf, wf), dtype=np.float32)
+        params = pkg.ConvParams(c, co, hf, wf, s)
+        ref = orc.conv_direct(inp, flt, s)
+        out = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path="fused").numpy()
+        assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (n, c, h, w, co, hf, wf, s)
