@@ -51,6 +51,27 @@ IM2WIN_DEVICE void cp_async_16(uint32_t dst, const void* src, uint32_t src_bytes
 
 IM2WIN_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 
+// mbarrier primitives for cp.async pipelines (SIMT kernels).
+IM2WIN_DEVICE void mbarrier_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+IM2WIN_DEVICE void mbarrier_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+IM2WIN_DEVICE void mbarrier_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Arrive on `bar` once all of this thread's prior cp.async copies have landed.
+IM2WIN_DEVICE void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
 template <int N>
 IM2WIN_DEVICE void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));

@@ -73,7 +73,7 @@ IM2WIN_DEVICE float mac(float acc, float a, float b) {
   }
 }
 
-template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC>
+template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC, bool MB = false>
 __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
     conv_simt_kernel(const ConvArgs a) {
   constexpr int NT = (BM / 8) * (BN / 8);
@@ -198,6 +198,44 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
       compute_stage(0);
       __syncthreads();
     }
+  } else if constexpr (MB) {
+    // mbarrier ring: full[s] completes when every thread's copies for the slab in
+    // slot s have landed (cp.async.mbarrier.arrive.noinc); empty[s] when every warp
+    // has consumed it.  No CTA-wide barrier in the K loop: warps may drift up to
+    // STAGES-PD-1 slabs apart.  PD+1 slabs are in flight ahead of the consumer.
+    constexpr int PD = STAGES - 3;
+    __shared__ __align__(8) uint64_t full_bar[STAGES];
+    __shared__ __align__(8) uint64_t empty_bar[STAGES];
+    if (tid == 0) {
+#pragma unroll
+      for (int s = 0; s < STAGES; ++s) {
+        mbarrier_init(&full_bar[s], NT);
+        mbarrier_init(&empty_bar[s], NT / 32);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s <= PD; ++s) {
+      if (s < k_tiles) {
+        load_stage(s, s);
+        cp_async_arrive_noinc(&full_bar[s]);
+      }
+    }
+    for (int kt = 0; kt < k_tiles; ++kt) {
+      const int pf = kt + PD + 1;
+      if (pf < k_tiles) {
+        const int ps = pf % STAGES;
+        if (pf >= STAGES) mbarrier_wait_parity(&empty_bar[ps], ((pf - STAGES) / STAGES) & 1);
+        load_stage(pf, ps);
+        cp_async_arrive_noinc(&full_bar[ps]);
+      }
+      const int slot = kt % STAGES;
+      mbarrier_wait_parity(&full_bar[slot], (kt / STAGES) & 1);
+      compute_stage(slot);
+      __syncwarp();
+      if ((tid & 31) == 0) mbarrier_arrive(&empty_bar[slot]);
+    }
   } else {
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -246,14 +284,14 @@ struct SimtConfig {
   int bm, bn, bk, stages;
 };
 
-template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC>
+template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC, bool MB = false>
 static cudaError_t launch_cfg(const ConvArgs& a0, cudaStream_t stream) {
   ConvArgs a = a0;
   a.m_tiles = (a.M + BM - 1) / BM;
   uint64_t n_tiles = (static_cast<uint64_t>(a.n_gemm) + BN - 1) / BN;
   uint64_t grid = n_tiles * a.m_tiles;
   size_t smem = static_cast<size_t>(STAGES) * BK * (BM + BN) * 4;
-  auto kern = conv_simt_kernel<BM, BN, BK, STAGES, EXACT, VEC>;
+  auto kern = conv_simt_kernel<BM, BN, BK, STAGES, EXACT, VEC, MB>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -280,7 +318,7 @@ extern "C" int im2win_simt_pick(int M, long long n_gemm, int K) {
 static const int kNumCfg = 7;
 static const int kBM[kNumCfg] = {128, 64, 96, 128, 64, 128, 64};
 static const int kBN[kNumCfg] = {128, 256, 128, 64, 256, 128, 256};
-static const int kBKc[kNumCfg] = {16, 16, 16, 16, 32, 32, 16};
+static const int kBKc[kNumCfg] = {16, 16, 16, 16, 16, 16, 16};
 static const int kMaxBK = 32;
 
 int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void* workspace,
@@ -330,18 +368,19 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
 
   cudaError_t e = cudaSuccess;
 #define IM2WIN_DISPATCH(BM_, BN_, BK_)                                                              \
-  if (exact && vec && stages == 3) e = launch_cfg<BM_, BN_, BK_, 3, true, true>(a, stream);          \
+  if (exact && vec && stages == 3) e = launch_cfg<BM_, BN_, BK_, 4, true, true, true>(a, stream);    \
   else if (exact && vec && stages == 1) e = launch_cfg<BM_, BN_, BK_, 1, true, true>(a, stream);     \
   else if (exact && !vec) e = launch_cfg<BM_, BN_, BK_, 3, true, false>(a, stream);                  \
-  else e = launch_cfg<BM_, BN_, BK_, 3, false, true>(a, stream);
+  else if (!exact && vec) e = launch_cfg<BM_, BN_, BK_, 4, false, true, true>(a, stream);           \
+  else e = launch_cfg<BM_, BN_, BK_, 3, false, false>(a, stream);
   switch (cfg) {
     case 0: { IM2WIN_DISPATCH(128, 128, 16) break; }
     case 1: { IM2WIN_DISPATCH(64, 256, 16) break; }
     case 2: { IM2WIN_DISPATCH(96, 128, 16) break; }
     case 3: { IM2WIN_DISPATCH(128, 64, 16) break; }
-    case 4: e = launch_cfg<64, 256, 32, 2, true, true>(a, stream); break;
-    case 5: e = launch_cfg<128, 128, 32, 2, true, true>(a, stream); break;
-    case 6: e = launch_cfg<64, 256, 16, 4, true, true>(a, stream); break;
+    case 4: e = launch_cfg<64, 256, 16, 3, true, true>(a, stream); break;     // __syncthreads ring (r01)
+    case 5: e = launch_cfg<128, 128, 16, 3, true, true>(a, stream); break;    // __syncthreads ring (r01)
+    case 6: e = launch_cfg<64, 256, 16, 5, true, true, true>(a, stream); break;  // deeper mbarrier ring
     default: *err = "im2win_conv_f32: unknown tile configuration"; return 1;
   }
 #undef IM2WIN_DISPATCH
