@@ -292,7 +292,7 @@ static cudaError_t launch_cfg(const ConvArgs& a0, cudaStream_t stream) {
   uint64_t grid = n_tiles * a.m_tiles;
   size_t smem = static_cast<size_t>(STAGES) * BK * (BM + BN) * 4;
   auto kern = conv_simt_kernel<BM, BN, BK, STAGES, EXACT, VEC, MB>;
-  if (smem > 48 * 1024) {
+  if (smem + 1024 > 48 * 1024) {  // + static smem (mbarriers)
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
