@@ -368,18 +368,18 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
 
   cudaError_t e = cudaSuccess;
 #define IM2WIN_DISPATCH(BM_, BN_, BK_)                                                              \
-  if (exact && vec && stages == 3) e = launch_cfg<BM_, BN_, BK_, 4, true, true, true>(a, stream);    \
+  if (exact && vec && stages == 3) e = launch_cfg<BM_, BN_, BK_, 3, true, true>(a, stream);          \
   else if (exact && vec && stages == 1) e = launch_cfg<BM_, BN_, BK_, 1, true, true>(a, stream);     \
   else if (exact && !vec) e = launch_cfg<BM_, BN_, BK_, 3, true, false>(a, stream);                  \
-  else if (!exact && vec) e = launch_cfg<BM_, BN_, BK_, 4, false, true, true>(a, stream);           \
+  else if (!exact && vec) e = launch_cfg<BM_, BN_, BK_, 3, false, true>(a, stream);               \
   else e = launch_cfg<BM_, BN_, BK_, 3, false, false>(a, stream);
   switch (cfg) {
     case 0: { IM2WIN_DISPATCH(128, 128, 16) break; }
     case 1: { IM2WIN_DISPATCH(64, 256, 16) break; }
     case 2: { IM2WIN_DISPATCH(96, 128, 16) break; }
     case 3: { IM2WIN_DISPATCH(128, 64, 16) break; }
-    case 4: e = launch_cfg<64, 256, 16, 3, true, true>(a, stream); break;     // __syncthreads ring (r01)
-    case 5: e = launch_cfg<128, 128, 16, 3, true, true>(a, stream); break;    // __syncthreads ring (r01)
+    case 4: e = launch_cfg<64, 256, 16, 4, true, true, true>(a, stream); break;   // mbarrier ring (explored)
+    case 5: e = launch_cfg<128, 128, 16, 4, true, true, true>(a, stream); break;  // mbarrier ring (explored)
     case 6: e = launch_cfg<64, 256, 16, 5, true, true, true>(a, stream); break;  // deeper mbarrier ring
     default: *err = "im2win_conv_f32: unknown tile configuration"; return 1;
   }
