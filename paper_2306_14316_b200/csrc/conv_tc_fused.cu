@@ -332,8 +332,13 @@ int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c
 size_t im2win_tc_fused_workspace_bytes(int64_t c_in, int64_t c_out, int h_f, int w_f) {
   const int64_t Mp = (c_out + 255) / 256 * 256 + 256;
   const int64_t Kfh = (w_f * c_in + 63) / 64 * 64;
-  return static_cast<size_t>(Mp * Kfh * h_f) * 4 + 1024;
+  const int64_t Kshift = static_cast<int64_t>(w_f) * ((c_in + 63) / 64 * 64);  // window-shift packing
+  return static_cast<size_t>(Mp * std::max(Kfh, Kshift) * h_f) * 4 + 1024;
 }
+
+int im2win_try_conv_tc_shift(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n, int64_t c_in,
+                             int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride, int bf16,
+                             double fused_util, cudaStream_t stream, const char** err);
 
 int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n,
                                 int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride,
@@ -372,6 +377,13 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
   a.n_tiles = (a.n_img + a.box_n - 1) / a.box_n;
   a.fh_slabs = static_cast<uint32_t>(Kfh / bk);
   a.k_slabs = a.fh_slabs * h_f;
+  {
+    // stride-1 layers: the window-shift kernel reuses each loaded A tile for all Wf taps
+    const double util = static_cast<double>(a.box_w) * a.box_h * a.box_n / kTileM;
+    const int rc = im2win_try_conv_tc_shift(x_cl, flt, out, workspace, n, c_in, h, w, c_out, h_f, w_f, stride, bf16,
+                                            util, stream, err);
+    if (rc != 0) return rc > 0 ? 0 : -rc;
+  }
   if (bf16)
     pack_filter_fused_kernel<true><<<256, 256, 0, stream>>>(flt, workspace, static_cast<int>(c_out),
                                                             static_cast<int>(c_in), h_f, w_f, static_cast<int>(Mp),
