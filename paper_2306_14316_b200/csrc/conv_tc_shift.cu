@@ -280,9 +280,9 @@ static int launch_shift(ShiftArgs a, const void* x_cl, const void* packed, int64
   }
   a.co_tiles = static_cast<uint32_t>(Mp / N);
   const size_t smem = static_cast<size_t>(STAGES) * (kARows + WF * N) * kRowBytes + 1024;
-  const char* env = getenv("IM2WIN_SHIFT_BASEOFF");
-  const bool baseoff = env ? atoi(env) != 0 : true;
-  auto kern = baseoff ? conv_tc_shift_kernel<BF16, N, STAGES, WF, true> : conv_tc_shift_kernel<BF16, N, STAGES, WF, false>;
+  // Measured on B200: the SW128 swizzle phase follows the absolute smem address, so the
+  // row-shifted start needs no descriptor base offset (BASEOFF=true gives wrong results).
+  auto kern = conv_tc_shift_kernel<BF16, N, STAGES, WF, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
@@ -325,9 +325,10 @@ int im2win_try_conv_tc_shift(const void* x_cl, const float* flt, float* out, voi
   a.co = static_cast<uint32_t>(c_out);
   const double util = shift_tile(n, h_out, w_out, w_f, a);
   if (util + 1e-9 < fused_util * 0.9) return 0;
-  // B per stage = Wf * N * 128 B must leave room for >= 3 stages: N <= 128 for Wf=3, N = 64 for Wf=5
-  int N = c_out <= 64 ? 64 : 128;
-  if (w_f == 5 && N > 64) return 0;
+  // B per stage = Wf * N * 128 B must leave room for >= 3 stages: N <= 128 for Wf=3, N = 64 for Wf=5.
+  // Wider Co would need a Co split (A re-read per split), measured slower than the generic kernel.
+  if (c_out > 128 || (w_f == 5 && c_out > 64)) return 0;
+  const int N = c_out <= 64 ? 64 : 128;
   const int bk = bf16 ? 64 : 32;
   const int64_t c_slabs = (c_in + bk - 1) / bk;
   const int64_t Kc = c_slabs * bk;
