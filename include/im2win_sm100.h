@@ -76,6 +76,13 @@ int im2win_conv_f32(const float* windows, const float* flt, float* out, int64_t 
                     int32_t w_f, int32_t stride, const im2win_tile_plan* plan, int32_t variant,
                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* Paper Alg. 2 basic kernel: one output per thread, operands from global memory
+ * (replaces _basic_window_kernel, kernels/reference.py:180-206, called at :215).
+ * Bit-exact like im2win_conv_f32 with IM2WIN_FP32_EXACT. */
+int im2win_conv_basic_f32(const float* windows, const float* flt, float* out, int64_t n,
+                          int64_t c_in, int64_t c_out, int64_t h_out, int64_t w_out,
+                          int64_t row_len, int32_t h_f, int32_t w_f, int32_t stride, void* stream);
+
 /* ---- Tensor-core fast path (extension; no counterpart in the reference) ----
  * The channels-innermost form of the window layout, Ĩcl[n*Ho+oh][col][fh][c] =
  * X[n][c][oh*stride+fh][col] (col < w_eff), makes every pixel's window one

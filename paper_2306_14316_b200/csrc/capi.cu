@@ -219,3 +219,23 @@ int im2win_conv_fused(const void* x_nhwc, const float* flt, float* out, int64_t 
 }
 
 }  // extern "C"
+
+// ---- paper Alg. 2 basic kernel (reference compute_from_windows_basic, reference.py:180-219) ----
+int im2win_launch_conv_basic(const float* win, const float* flt, float* out, int64_t n, int64_t c_in, int64_t c_out,
+                             int64_t h_out, int64_t w_out, int64_t row_len, int h_f, int w_f, int stride,
+                             cudaStream_t stream, const char** err);
+
+extern "C" int im2win_conv_basic_f32(const float* windows, const float* flt, float* out, int64_t n, int64_t c_in,
+                                     int64_t c_out, int64_t h_out, int64_t w_out, int64_t row_len, int32_t h_f,
+                                     int32_t w_f, int32_t stride, void* stream) {
+  g_last_error[0] = '\0';
+  if (!windows || !flt || !out) return fail(1, "im2win_conv_basic_f32: null pointer");
+  if (n < 1 || c_in < 1 || c_out < 1 || h_out < 1 || w_out < 1 || h_f < 1 || w_f < 1 || stride < 1)
+    return fail(1, "im2win_conv_basic_f32: extents must be positive");
+  if (row_len != h_f * ((w_out - 1) * stride + w_f)) return fail(1, "im2win_conv_basic_f32: row_len != h_f * w_eff");
+  if (int rc = bind_device_of(out)) return rc;
+  const char* err = nullptr;
+  int rc = im2win_launch_conv_basic(windows, flt, out, n, c_in, c_out, h_out, w_out, row_len, h_f, w_f, stride,
+                                    static_cast<cudaStream_t>(stream), &err);
+  return rc ? fail(rc, err) : 0;
+}

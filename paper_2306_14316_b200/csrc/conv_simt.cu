@@ -519,3 +519,63 @@ int im2win_launch_conv_simt_1x1(const float* win, const float* flt, float* out, 
   if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 2; }
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// Paper Alg. 2 "basic" im2win kernel (winconv
+// _basic_window_kernel, reference.py:180-206): grid (N/32, M/32), block 32x32,
+// one output per thread, operands read straight from global memory through the
+// window map Ĩ[n, c, oh, (ow*s + fw)*Hf + fh] -- no shared-memory tiling, no
+// register micro-tile.  Same unfused ascending-k arithmetic (bit-exact); it is the
+// baseline the tiled kernel is measured against (reference test_acceptance.py:185-215).
+// ---------------------------------------------------------------------------
+namespace im2win {
+
+__global__ void __launch_bounds__(1024) conv_basic_kernel(const float* __restrict__ win, const float* __restrict__ flt,
+                                                          float* __restrict__ out, uint32_t n_gemm, uint32_t M,
+                                                          uint32_t K, uint32_t c_in, uint32_t h_out, uint32_t row_len,
+                                                          uint32_t h_f, uint32_t w_f, uint32_t s_hf, FastDiv fd_hw,
+                                                          FastDiv fd_wo, uint32_t hw) {
+  const uint32_t n = blockIdx.x * 32 + threadIdx.x;
+  const uint32_t m = blockIdx.y * 32 + threadIdx.y;
+  if (n >= n_gemm || m >= M) return;
+  uint32_t img, rem, oh, ow;
+  fd_hw.divmod(n, img, rem);
+  fd_wo.divmod(rem, oh, ow);
+  const float* wp = win + (static_cast<int64_t>(img) * c_in * h_out + oh) * row_len + static_cast<int64_t>(ow) * s_hf;
+  const float* fp = flt + static_cast<int64_t>(m) * K;
+  const int64_t chan = static_cast<int64_t>(h_out) * row_len;
+  float acc = 0.0f;
+  uint32_t k = 0;
+  for (uint32_t c = 0; c < c_in; ++c) {
+    for (uint32_t fh = 0; fh < h_f; ++fh) {
+      for (uint32_t fw = 0; fw < w_f; ++fw, ++k) acc = __fadd_rn(acc, __fmul_rn(__ldg(fp + k), __ldg(wp + fw * h_f + fh)));
+    }
+    wp += chan;
+  }
+  out[static_cast<int64_t>(img) * M * hw + static_cast<int64_t>(m) * hw + rem] = acc;
+}
+
+}  // namespace im2win
+
+int im2win_launch_conv_basic(const float* win, const float* flt, float* out, int64_t n, int64_t c_in, int64_t c_out,
+                             int64_t h_out, int64_t w_out, int64_t row_len, int h_f, int w_f, int stride,
+                             cudaStream_t stream, const char** err) {
+  using namespace im2win;
+  const int64_t hw = h_out * w_out, n_gemm = n * hw, K = c_in * h_f * w_f;
+  if (n_gemm >= (1ll << 31) || (n_gemm + 31) / 32 >= (1ll << 31) || (c_out + 31) / 32 > 65535) {
+    *err = "im2win_conv_basic_f32: extents exceed the kernel's index range";
+    return 1;
+  }
+  dim3 grid(static_cast<unsigned>((n_gemm + 31) / 32), static_cast<unsigned>((c_out + 31) / 32));
+  conv_basic_kernel<<<grid, dim3(32, 32), 0, stream>>>(
+      win, flt, out, static_cast<uint32_t>(n_gemm), static_cast<uint32_t>(c_out), static_cast<uint32_t>(K),
+      static_cast<uint32_t>(c_in), static_cast<uint32_t>(h_out), static_cast<uint32_t>(row_len), h_f, w_f,
+      static_cast<uint32_t>(stride * h_f), FastDiv(static_cast<uint32_t>(hw)), FastDiv(static_cast<uint32_t>(w_out)),
+      static_cast<uint32_t>(hw));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 2;
+  }
+  return 0;
+}

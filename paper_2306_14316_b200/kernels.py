@@ -85,6 +85,40 @@ def compute_from_windows_opt(windows: Im2winTensor, flt, params: ConvParams,
     return Tensor4(out)
 
 
+def basic_windows_into(win: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, params: ConvParams) -> None:
+    """Paper Alg. 2 basic kernel into a caller-allocated output (reference.py:209-219 seam)."""
+    n_img, c_in, h_out, row_len = (int(d) for d in win.shape)
+    w_out = int(out.shape[3])
+    with torch.cuda.device(win.device):
+        rc = _lib.load().im2win_conv_basic_f32(
+            win.data_ptr(), flt.data_ptr(), out.data_ptr(), n_img, c_in, params.c_out, h_out, w_out, row_len,
+            params.h_f, params.w_f, params.stride, torch.cuda.current_stream(win.device).cuda_stream)
+    _lib.check(rc)
+
+
+def compute_from_windows_basic(windows: Im2winTensor, flt, params: ConvParams) -> Tensor4:
+    """Basic window-order convolution on an already-transformed input (reference.py:209-219)."""
+    f = flt if isinstance(flt, Tensor4) else Tensor4(flt)
+    if f.dims != params.filter_dims:
+        raise ShapeError(f"filter dims {f.dims} do not match params {params.filter_dims}")
+    if windows.c_in != params.c_in or (windows.h_f, windows.w_f, windows.stride) != (params.h_f, params.w_f,
+                                                                                       params.stride):
+        raise ShapeError("window tensor geometry does not match params")
+    fd = f.data if f.device == windows.data.device else f.data.to(windows.data.device)
+    out = torch.empty((windows.n, params.c_out, windows.h_out, windows.w_out), dtype=DTYPE,
+                      device=windows.data.device)
+    basic_windows_into(windows.data, fd, out, params)
+    return Tensor4(out)
+
+
+def conv_im2win_basic(inp, flt, params: ConvParams) -> Tensor4:
+    """Window-order transform followed by one thread per output element (reference.py:222-225)."""
+    i = inp if isinstance(inp, Tensor4) else Tensor4(inp)
+    f = flt if isinstance(flt, Tensor4) else Tensor4(flt)
+    check_conv_operands(i, f, params)
+    return compute_from_windows_basic(im2win(i, params), f, params)
+
+
 def cl_supported(c_in: int, variant: str) -> bool:
     """The channels-innermost TMA path needs c_in * element size to be a multiple of 16 bytes."""
     if variant == "tf32":

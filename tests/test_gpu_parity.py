@@ -201,3 +201,24 @@ def test_tc_fused_odd_geometries(variant):
         ref = orc.conv_direct(inp, flt, s)
         out = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path="fused").numpy()
         assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (n, c, h, w, co, hf, wf, s)
+
+
+def test_basic_kernel_bitwise(small_cases):
+    """Paper Alg. 2 basic kernel (reference compute_from_windows_basic) is bit-exact too."""
+    for name in ["fig1", "special", "identity1x1"] + [f"rand{i:03d}" for i in range(0, 200, 3)]:
+        c = small_cases[name]
+        out = pkg.conv_im2win_basic(torch.from_numpy(c["inp"]).to(DEV), torch.from_numpy(c["flt"]).to(DEV), _params(c))
+        assert bits_equal_nan_as_class(out.numpy(), c["out"]), name
+
+
+def test_harness_records_and_csv():
+    from paper_2306_14316_b200 import harness
+    cfg = replace(BENCHMARKS["conv10"], batch=4, seed=5)
+    recs = [harness.run_bench(cfg, a, repeats=2) for a in ("im2win-opt", "im2win-basic", "im2win-bf16", "cudnn")]
+    assert recs[0].checksum == recs[1].checksum          # exact kernels agree bitwise
+    assert all(r.tflops > 0 and r.total_s > 0 for r in recs)
+    abl = harness.run_ablation(cfg, repeats=2)
+    assert [r.variant for r in abl] == list(harness.ABLATION_VARIANTS)
+    assert len({r.checksum for r in abl}) == 1 and abl[0].checksum == recs[0].checksum
+    csv = harness.report_csv(recs + abl)
+    assert csv.splitlines()[0].split(",")[:17] == list(harness.CSV_COLUMNS[:17])
