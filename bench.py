@@ -409,7 +409,7 @@ def main() -> None:
     # ---- tensor-core variants (rank 0): TF32 / BF16 per layer at N=128 and config 4 ----
     tc = None
     if rank == 0 and not args.no_tc:
-        from paper_2306_14316_b200.kernels import cl_supported, conv_fused_into, nhwc_into
+        from paper_2306_14316_b200.kernels import conv_fused_into, nhwc_into, nhwc_pitch
 
         def tc_layer(cfg, v):
             """transform + conv time (ms) of the production TC path for one layer."""
@@ -418,17 +418,13 @@ def main() -> None:
             x = torch.randn((cfg.batch, cfg.c_in, cfg.h_in, cfg.w_in), device=dev, generator=g2)
             f = torch.randn((cfg.c_out, cfg.c_in, cfg.h_f, cfg.w_f), device=dev, generator=g2)
             o = torch.empty((cfg.batch, cfg.c_out, h_out, w_out), device=dev)
-            if cl_supported(cfg.c_in, v):
-                w = torch.empty((cfg.batch, cfg.h_in, cfg.w_in, cfg.c_in),
-                                dtype=torch.bfloat16 if v == "bf16" else torch.float32, device=dev)
-                tr = lambda: nhwc_into(x, w)  # noqa: E731
-                cv = lambda: conv_fused_into(w, f, o, cfg.params, v)  # noqa: E731
-                path = "fused: NHWC copy + 5-D TMA window boxes -> tcgen05"
-            else:
-                w = torch.empty((cfg.batch, cfg.c_in, h_out, cfg.h_f * cfg.w_eff), device=dev)
-                tr = lambda: im2win_into(x, w, cfg.params)  # noqa: E731
-                cv = lambda: conv_windows_into(w, f, o, cfg.params, cfg.w_eff, None, v)  # noqa: E731
-                path = "im2win + gathered tcgen05"
+            # the fused path covers every layer (channel pitch padded to a 16 B multiple)
+            w = torch.empty((cfg.batch, cfg.h_in, cfg.w_in, nhwc_pitch(cfg.c_in, v)),
+                            dtype=torch.bfloat16 if v == "bf16" else torch.float32, device=dev)
+            tr = lambda: nhwc_into(x, w)  # noqa: E731
+            cv = lambda: conv_fused_into(w, f, o, cfg.params, v)  # noqa: E731
+            path = ("fused+shift" if cfg.stride == 1 and cfg.w_f in (3, 5) and cfg.c_out <= 128 else "fused") + \
+                ": NHWC copy + TMA window boxes -> tcgen05"
             tr()
             cv()
             best_t = best_c = 1e30

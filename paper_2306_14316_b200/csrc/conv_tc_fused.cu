@@ -22,11 +22,12 @@
 namespace im2win {
 namespace tc {
 
-// NCHW float32 -> NHWC (float32 or bf16): per image a [C][H*W] -> [H*W][C] transpose.
+// NCHW float32 -> NHWC (float32 or bf16) with the channel pitch padded to c_pad
+// (a 16-byte multiple, zero filled): per image a [C][H*W] -> [H*W][c_pad] transpose.
 template <bool BF16>
 __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restrict__ src, void* __restrict__ dst,
-                                                           uint32_t c_in, uint32_t hw, uint32_t hw_tiles,
-                                                           uint32_t c_tiles, uint32_t total) {
+                                                           uint32_t c_in, uint32_t c_pad, uint32_t hw,
+                                                           uint32_t hw_tiles, uint32_t c_tiles, uint32_t total) {
   __shared__ float tile[32][33];
   const uint32_t tx = threadIdx.x % 32, ty = threadIdx.x / 32;
   for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
@@ -44,9 +45,9 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restri
     // write: 8 threads per pixel, 4 channels each (16 B fp32 / 8 B bf16)
     const uint32_t pl = threadIdx.x / 8, cq = threadIdx.x % 8;
     const uint32_t p = p0 + pl, c = c0 + cq * 4;
-    if (p < hw && c < c_in) {
+    if (p < hw && c < c_pad) {
       const float v0 = tile[cq * 4][pl], v1 = tile[cq * 4 + 1][pl], v2 = tile[cq * 4 + 2][pl], v3 = tile[cq * 4 + 3][pl];
-      const uint64_t o = (static_cast<uint64_t>(img) * hw + p) * c_in + c;
+      const uint64_t o = (static_cast<uint64_t>(img) * hw + p) * c_pad + c;
       if constexpr (BF16) {
         uint2 q;
         q.x = pack_bf16x2(v0, v1);
@@ -209,10 +210,11 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-// B[m][fh*Kfh + j] = F[m][c][fh][fw] for j = fw*C + c < Wf*C, zero elsewhere.
+// B[m][fh*Kfh + j] = F[m][c][fh][fw] for j = fw*CP + c (c < C real channels, CP = padded
+// channel pitch of the NHWC copy), zero elsewhere.
 template <bool BF16>
 __global__ void pack_filter_fused_kernel(const float* __restrict__ flt, void* __restrict__ packed, int M, int C,
-                                         int h_f, int w_f, int Mp, int Kfh, int Kp) {
+                                         int CP, int h_f, int w_f, int Mp, int Kfh, int Kp) {
   const int64_t total = static_cast<int64_t>(Mp) * Kp;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -220,10 +222,8 @@ __global__ void pack_filter_fused_kernel(const float* __restrict__ flt, void* __
     const int kp = static_cast<int>(i % Kp);
     const int fh = kp / Kfh, j = kp % Kfh;
     float v = 0.0f;
-    if (m < M && j < w_f * C) {
-      const int fw = j / C, c = j % C;
-      v = flt[((static_cast<int64_t>(m) * C + c) * h_f + fh) * w_f + fw];
-    }
+    const int fw = j / CP, c = j % CP;
+    if (m < M && fw < w_f && c < C) v = flt[((static_cast<int64_t>(m) * C + c) * h_f + fh) * w_f + fw];
     if constexpr (BF16) {
       reinterpret_cast<__nv_bfloat16*>(packed)[i] = __float2bfloat16_rn(v);
     } else {
@@ -299,24 +299,33 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
 }  // namespace tc
 }  // namespace im2win
 
+// Channel pitch of the NHWC copy: the smallest 16-byte multiple >= c (TMA stride rule).
+int64_t im2win_nhwc_channel_pitch(int64_t c, int bf16) {
+  const int64_t q = bf16 ? 8 : 4;
+  return (c + q - 1) / q * q;
+}
+
 int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w, int bf16,
                                cudaStream_t stream, const char** err) {
   const int64_t hw = h * w;
-  const int64_t hw_tiles = (hw + 31) / 32, c_tiles = (c + 31) / 32;
+  const int64_t cp = im2win_nhwc_channel_pitch(c, bf16);
+  const int64_t hw_tiles = (hw + 31) / 32, c_tiles = (cp + 31) / 32;
   const int64_t total = n * hw_tiles * c_tiles;
-  if (c % 4 != 0 || total >= (1ll << 32) || hw >= (1ll << 31)) {
-    *err = "nchw_to_nhwc: c must be a multiple of 4 and extents within range";
+  if (total >= (1ll << 32) || hw >= (1ll << 31)) {
+    *err = "nchw_to_nhwc: extents exceed the kernel's index range";
     return 1;
   }
   const uint32_t grid = static_cast<uint32_t>(total < 148 * 16 ? total : 148 * 16);
   if (bf16)
     im2win::tc::nchw_to_nhwc_kernel<true><<<grid, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
+                                                                     static_cast<uint32_t>(cp),
                                                                      static_cast<uint32_t>(hw),
                                                                      static_cast<uint32_t>(hw_tiles),
                                                                      static_cast<uint32_t>(c_tiles),
                                                                      static_cast<uint32_t>(total));
   else
     im2win::tc::nchw_to_nhwc_kernel<false><<<grid, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
+                                                                      static_cast<uint32_t>(cp),
                                                                       static_cast<uint32_t>(hw),
                                                                       static_cast<uint32_t>(hw_tiles),
                                                                       static_cast<uint32_t>(c_tiles),
@@ -330,6 +339,7 @@ int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c
 }
 
 size_t im2win_tc_fused_workspace_bytes(int64_t c_in, int64_t c_out, int h_f, int w_f) {
+  c_in = im2win_nhwc_channel_pitch(c_in, 1);  // >= either pitch
   const int64_t Mp = (c_out + 255) / 256 * 256 + 256;
   const int64_t Kfh = (w_f * c_in + 63) / 64 * 64;
   const int64_t Kshift = static_cast<int64_t>(w_f) * ((c_in + 63) / 64 * 64);  // window-shift packing
@@ -337,22 +347,18 @@ size_t im2win_tc_fused_workspace_bytes(int64_t c_in, int64_t c_out, int h_f, int
 }
 
 int im2win_try_conv_tc_shift(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n, int64_t c_in,
-                             int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride, int bf16,
+                             int64_t c_pad, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride, int bf16,
                              double fused_util, cudaStream_t stream, const char** err);
 
 int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n,
                                 int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride,
                                 int bf16, cudaStream_t stream, const char** err) {
   using namespace im2win::tc;
-  const int64_t esz = bf16 ? 2 : 4;
-  if ((c_in * esz) % 16 != 0) {
-    *err = "im2win_conv_fused: c_in * element size must be a multiple of 16 bytes";
-    return 1;
-  }
+  const int64_t cp = im2win_nhwc_channel_pitch(c_in, bf16);  // channel pitch of x_cl
   const int64_t h_out = (h - h_f) / stride + 1, w_out = (w - w_f) / stride + 1;
   const int N = c_out <= 64 ? 64 : c_out <= 96 ? 96 : c_out <= 128 ? 128 : 256;
   const int bk = bf16 ? 64 : 32;
-  const int64_t Kfh = (w_f * c_in + bk - 1) / bk * bk;
+  const int64_t Kfh = (w_f * cp + bk - 1) / bk * bk;
   const int64_t Kp = Kfh * h_f;
   const int64_t Mp = (c_out + N - 1) / N * N;
   FusedArgs a{};
@@ -380,20 +386,22 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
   {
     // stride-1 layers: the window-shift kernel reuses each loaded A tile for all Wf taps
     const double util = static_cast<double>(a.box_w) * a.box_h * a.box_n / kTileM;
-    const int rc = im2win_try_conv_tc_shift(x_cl, flt, out, workspace, n, c_in, h, w, c_out, h_f, w_f, stride, bf16,
-                                            util, stream, err);
+    const int rc = im2win_try_conv_tc_shift(x_cl, flt, out, workspace, n, c_in, cp, h, w, c_out, h_f, w_f, stride,
+                                            bf16, util, stream, err);
     if (rc != 0) return rc > 0 ? 0 : -rc;
   }
   if (bf16)
     pack_filter_fused_kernel<true><<<256, 256, 0, stream>>>(flt, workspace, static_cast<int>(c_out),
-                                                            static_cast<int>(c_in), h_f, w_f, static_cast<int>(Mp),
-                                                            static_cast<int>(Kfh), static_cast<int>(Kp));
+                                                            static_cast<int>(c_in), static_cast<int>(cp), h_f, w_f,
+                                                            static_cast<int>(Mp), static_cast<int>(Kfh),
+                                                            static_cast<int>(Kp));
   else
     pack_filter_fused_kernel<false><<<256, 256, 0, stream>>>(flt, workspace, static_cast<int>(c_out),
-                                                             static_cast<int>(c_in), h_f, w_f, static_cast<int>(Mp),
-                                                             static_cast<int>(Kfh), static_cast<int>(Kp));
+                                                             static_cast<int>(c_in), static_cast<int>(cp), h_f, w_f,
+                                                             static_cast<int>(Mp), static_cast<int>(Kfh),
+                                                             static_cast<int>(Kp));
 #define IM2WIN_FU(BF, NN, ST) \
-  return launch_fused<BF, NN, ST>(a, x_cl, workspace, c_in, h, w, h_f, w_f, stride, Kp, Mp, stream, err)
+  return launch_fused<BF, NN, ST>(a, x_cl, workspace, cp, h, w, h_f, w_f, stride, Kp, Mp, stream, err)
   if (bf16) {
     switch (N) {
       case 64: IM2WIN_FU(true, 64, 8);

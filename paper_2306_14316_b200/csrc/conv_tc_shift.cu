@@ -309,7 +309,7 @@ static int launch_shift(ShiftArgs a, const void* x_cl, const void* packed, int64
 // utilisation not worse than the generic fused tile), 0 when the caller should use the
 // generic fused kernel, <0 on error.
 int im2win_try_conv_tc_shift(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n, int64_t c_in,
-                             int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride, int bf16,
+                             int64_t c_pad, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride, int bf16,
                              double fused_util, cudaStream_t stream, const char** err) {
   using namespace im2win::tc;
   if (stride != 1 || (w_f != 3 && w_f != 5)) return 0;
@@ -349,7 +349,7 @@ int im2win_try_conv_tc_shift(const void* x_cl, const float* flt, float* out, voi
                                                              static_cast<int>(c_in), h_f, w_f, static_cast<int>(Mp),
                                                              static_cast<int>(Kc));
   int rc;
-#define IM2WIN_SH(BF, NN, ST, WFF) rc = launch_shift<BF, NN, ST, WFF>(a, x_cl, workspace, c_in, h, w, Mp, Kp, stream, err)
+#define IM2WIN_SH(BF, NN, ST, WFF) rc = launch_shift<BF, NN, ST, WFF>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err)
   if (w_f == 3) {
     if (bf16) { if (N == 64) IM2WIN_SH(true, 64, 5, 3); else IM2WIN_SH(true, 128, 3, 3); }
     else { if (N == 64) IM2WIN_SH(false, 64, 5, 3); else IM2WIN_SH(false, 128, 3, 3); }

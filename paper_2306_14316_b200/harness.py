@@ -19,7 +19,7 @@ import torch
 import torch.nn.functional as F
 
 from .errors import MemoryBudgetError
-from .kernels import (basic_windows_into, cl_supported, conv_fused_into, conv_windows_into, nhwc_into)
+from .kernels import basic_windows_into, conv_fused_into, conv_windows_into, nhwc_into, nhwc_pitch
 from .layouts import im2win_into
 from .plan import TilePlan, gpu_plan
 from .workloads import BENCHMARKS, BenchConfig
@@ -94,20 +94,18 @@ def _stages(cfg: BenchConfig, algorithm: str, x, f, plan: TilePlan | None):
     p = cfg.params
     h_out, w_out = cfg.out_dims
     out = torch.empty((cfg.batch, cfg.c_out, h_out, w_out), device=x.device)
-    if algorithm in ("im2win-opt", "im2win-basic", "im2win-fma") or (
-            algorithm in ("im2win-tf32", "im2win-bf16") and not cl_supported(cfg.c_in, algorithm[7:])):
+    if algorithm in ("im2win-opt", "im2win-basic", "im2win-fma"):
         win = torch.empty((cfg.batch, cfg.c_in, h_out, cfg.h_f * cfg.w_eff), device=x.device)
         tr = lambda: im2win_into(x, win, p)  # noqa: E731
         if algorithm == "im2win-basic":
             cv = lambda: basic_windows_into(win, f, out, p)  # noqa: E731
         else:
-            variant = {"im2win-opt": "fp32-exact", "im2win-fma": "fp32-fma", "im2win-tf32": "tf32",
-                       "im2win-bf16": "bf16"}[algorithm]
+            variant = "fp32-exact" if algorithm == "im2win-opt" else "fp32-fma"
             cv = lambda: conv_windows_into(win, f, out, p, cfg.w_eff, plan, variant)  # noqa: E731
         return tr, cv, out
     if algorithm in ("im2win-tf32", "im2win-bf16"):
         variant = algorithm[7:]
-        xc = torch.empty((cfg.batch, cfg.h_in, cfg.w_in, cfg.c_in), device=x.device,
+        xc = torch.empty((cfg.batch, cfg.h_in, cfg.w_in, nhwc_pitch(cfg.c_in, variant)), device=x.device,
                          dtype=torch.bfloat16 if variant == "bf16" else torch.float32)
         return (lambda: nhwc_into(x, xc)), (lambda: conv_fused_into(xc, f, out, p, variant)), out
     if algorithm == "cudnn":

@@ -172,10 +172,17 @@ def nhwc_into(src: torch.Tensor, dst: torch.Tensor) -> None:
     _lib.check(rc)
 
 
+def nhwc_pitch(c_in: int, variant: str) -> int:
+    """Channel pitch of the channels-last copy: the smallest 16-byte multiple >= c_in."""
+    q = 8 if variant == "bf16" else 4
+    return -(-c_in // q) * q
+
+
 def conv_fused_into(x_nhwc: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, params: ConvParams,
                     variant: str) -> None:
     """tcgen05 convolution whose window tiles TMA builds from the channels-last input."""
-    n_img, h_in, w_in, c_in = (int(d) for d in x_nhwc.shape)
+    n_img, h_in, w_in, _pitch = (int(d) for d in x_nhwc.shape)
+    c_in = params.c_in
     code = _variant_code(variant)
     lib = _lib.load()
     nbytes = lib.im2win_conv_fused_workspace_bytes(params.c_in, params.c_out, params.h_f, params.w_f)
@@ -198,8 +205,9 @@ def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, 
     FP32 variants use the reference window layout Ĩ.  Tensor-core variants pick
     (tc_path="auto"): "fused" — TMA builds window tiles from a channels-last copy
     of the input (no Ĩ); "cl" — materialised channels-innermost Ĩ streamed by TMA;
-    "gather" — reference Ĩ gathered by producer warps.  fused/cl need
-    c_in * element size to be a multiple of 16 bytes; otherwise gather is used.
+    "gather" — reference Ĩ gathered by producer warps.  The fused copy pads the
+    channel pitch to a 16-byte multiple (zeros); "cl" needs c_in * element size
+    to be a multiple of 16 bytes and otherwise falls back to gather.
     """
     if tc_path not in TC_PATHS:
         raise ValueError(f"tc_path must be one of {TC_PATHS}")
@@ -207,10 +215,10 @@ def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, 
     f = flt if isinstance(flt, Tensor4) else Tensor4(flt)
     h_out, w_out = check_conv_operands(i, f, params)
     ok = cl_supported(params.c_in, variant)
-    if ok and tc_path in ("auto", "fused"):
+    if variant in ("tf32", "bf16") and tc_path in ("auto", "fused"):
         dt = torch.bfloat16 if variant == "bf16" else torch.float32
         n_img, c_in, h_in, w_in = i.dims
-        x_cl = torch.empty((n_img, h_in, w_in, c_in), dtype=dt, device=i.device)
+        x_cl = torch.empty((n_img, h_in, w_in, nhwc_pitch(c_in, variant)), dtype=dt, device=i.device)
         nhwc_into(i.data, x_cl)
         out = torch.empty((n_img, params.c_out, h_out, w_out), dtype=DTYPE, device=i.device)
         fd = f.data if f.device == i.device else f.data.to(i.device)

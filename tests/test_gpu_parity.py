@@ -222,3 +222,18 @@ def test_harness_records_and_csv():
     assert len({r.checksum for r in abl}) == 1 and abl[0].checksum == recs[0].checksum
     csv = harness.report_csv(recs + abl)
     assert csv.splitlines()[0].split(",")[:17] == list(harness.CSV_COLUMNS[:17])
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_tc_fused_padded_channels(variant):
+    """C not a multiple of 16 bytes (C=3 layers conv1/2/3/7, C=5, C=6): the channels-last
+    copy pads the channel pitch with zeros and the fused/shift kernels still apply."""
+    rng = np.random.default_rng(33)
+    for (n, c, h, w, co, hf, wf, s) in [(2, 3, 227, 227, 96, 11, 11, 4), (2, 3, 40, 44, 64, 3, 3, 1),
+                                        (3, 5, 17, 19, 20, 5, 5, 1), (2, 6, 21, 20, 33, 7, 7, 2)]:
+        inp = rng.standard_normal((n, c, h, w), dtype=np.float32)
+        flt = rng.standard_normal((co, c, hf, wf), dtype=np.float32)
+        params = pkg.ConvParams(c, co, hf, wf, s)
+        ref = orc.conv_direct(inp, flt, s)
+        out = pkg.conv_im2win_opt(inp, flt, params, variant=variant).numpy()
+        assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (c, hf, s)
