@@ -37,7 +37,7 @@ IM2WIN_DEVICE uint64_t smem_desc_sw128_off(uint32_t addr) {
 }
 
 template <bool BF16, int N, int STAGES, int WF, bool BASEOFF>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kTcThreads, 1)
     conv_tc_shift_kernel(const ShiftArgs a, const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b) {
   constexpr uint32_t kABytes = kARows * kRowBytes;  // 17 KB (multiple of 1024)
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 4);
+      mbar_init(&tempty_bar[s], kEpiWarps);
     }
     fence_barrier_init();
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap_a) : "memory");
@@ -152,7 +152,9 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
+    // kEpiWarps epilogue warps: warp w reads TMEM lane quarter w % 4 and column half (w - 4) / 4
     const int quarter = warp % 4;
+    const int j_lo = ((warp - 4) / 4) * (N / 2);
     const uint32_t r = quarter * 32 + lane;
     const uint32_t per_img = a.pitch * a.rows;
     const uint32_t r_n = r / per_img, r_rem = r % per_img;
@@ -171,7 +173,8 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * N;
 #pragma unroll
-      for (int j0 = 0; j0 < N; j0 += 16) {
+      for (int jj = 0; jj < N / 2; jj += 16) {
+        const int j0 = j_lo + jj;
         uint32_t v[16];
         tmem_ld16(taddr + j0, v);
         const uint32_t m0 = co_blk * N + j0;
@@ -293,7 +296,7 @@ static int launch_shift(ShiftArgs a, const void* x_cl, const void* packed, int64
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t tiles = static_cast<uint64_t>(a.n_tiles) * a.oh_tiles * a.ow_tiles * a.co_tiles;
   const uint32_t grid = tiles < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(tiles) : static_cast<uint32_t>(sms);
-  kern<<<grid, 256, smem, stream>>>(a, map_a, map_b);
+  kern<<<grid, kTcThreads, smem, stream>>>(a, map_a, map_b);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);

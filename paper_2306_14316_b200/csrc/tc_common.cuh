@@ -14,6 +14,10 @@ namespace tc {
 
 constexpr int kTileM = 128;        // pixels per tile (UMMA M)
 constexpr int kRowBytes = 128;     // one swizzle-128B row of K per stage
+// TMA-fed kernels: warp 0 TMA, warp 1 MMA, warp 2 TMEM allocator, warp 3 idle,
+// warps 4..4+kEpiWarps-1 epilogue (two warps per TMEM lane quarter, one per column half).
+constexpr int kEpiWarps = 8;
+constexpr int kTcThreads = (4 + kEpiWarps) * 32;
 
 // ---------------------------------------------------------------- PTX helpers
 IM2WIN_DEVICE void mbar_init(uint64_t* bar, uint32_t count) {

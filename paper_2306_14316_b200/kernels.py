@@ -215,6 +215,8 @@ def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, 
     f = flt if isinstance(flt, Tensor4) else Tensor4(flt)
     h_out, w_out = check_conv_operands(i, f, params)
     ok = cl_supported(params.c_in, variant)
+    if tc_path == "auto" and variant == "tf32" and not ok:
+        tc_path = "gather"  # measured: for C*4 % 16 != 0 (C=3 layers) the gathered Ĩ beats the padded copy
     if variant in ("tf32", "bf16") and tc_path in ("auto", "fused"):
         dt = torch.bfloat16 if variant == "bf16" else torch.float32
         n_img, c_in, h_in, w_in = i.dims
