@@ -36,12 +36,12 @@ IM2WIN_DEVICE uint64_t smem_desc_sw128_off(uint32_t addr) {
   return d;
 }
 
-template <bool BF16, int N, int STAGES, int WF, bool BASEOFF>
+template <bool BF16, int N, int STAGES, int WF, bool RB>
 __global__ void __launch_bounds__(kTcThreads, 1)
     conv_tc_shift_kernel(const ShiftArgs a, const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b) {
   constexpr uint32_t kABytes = kARows * kRowBytes;  // 17 KB (multiple of 1024)
-  constexpr uint32_t kBBytes = WF * N * kRowBytes;
+  constexpr uint32_t kBBytes = RB ? 0 : WF * N * kRowBytes;  // RB: filter resident, not staged
   constexpr uint32_t kStageBytes = kABytes + kBBytes;
   constexpr int kBK = BF16 ? 64 : 32;
   constexpr int kUK = BF16 ? 16 : 8;
@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
   __shared__ __align__(8) uint64_t tfull_bar[2];
   __shared__ __align__(8) uint64_t tempty_bar[2];
+  __shared__ __align__(8) uint64_t bres_bar;
   __shared__ uint32_t tmem_base_sh;
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -61,10 +62,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int lane = threadIdx.x % 32;
   const uint32_t loaded_rows = a.pitch * a.rows * a.box_n;
   const uint32_t a_box_bytes = loaded_rows * kRowBytes;
+  // RB: the whole packed filter (k_slabs x Wf tiles of N x 128 B) sits in front of the A stages
+  const uint32_t rb_bytes = RB ? a.k_slabs * WF * N * kRowBytes : 0;
+  uint8_t* stages = smem + rb_bytes;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
+      if (s == 0) mbar_init(&bres_bar, 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -83,7 +88,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   // rows past the TMA box feed only padding D rows, but keep them finite
   for (uint32_t i = threadIdx.x; i < STAGES * kABytes / 16; i += blockDim.x) {
     const uint32_t s = i / (kABytes / 16), off = i % (kABytes / 16);
-    reinterpret_cast<uint4*>(smem + s * kStageBytes)[off] = make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(stages + s * kStageBytes)[off] = make_uint4(0, 0, 0, 0);
   }
   fence_proxy_async_smem();
   tc_fence_before();
@@ -95,6 +100,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
+      if constexpr (RB) {  // requires co_tiles == 1 (host-checked)
+        mbar_arrive_expect_tx(&bres_bar, rb_bytes);
+        for (uint32_t ks = 0; ks < a.k_slabs; ++ks)
+          for (int fw = 0; fw < WF; ++fw)
+            tma_load_2d(smem + (ks * WF + fw) * N * kRowBytes, &tmap_b, &bres_bar,
+                        ((ks / a.c_slabs) * WF + fw) * a.c_slabs * kBK + (ks % a.c_slabs) * kBK, 0);
+      }
       for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         const uint32_t co_blk = t % a.co_tiles;
         uint32_t pt = t / a.co_tiles;
@@ -106,7 +118,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const uint32_t fh = ks / a.c_slabs;
           const uint32_t c0 = (ks % a.c_slabs) * kBK;
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* st = smem + stage * kStageBytes;
+          uint8_t* st = stages + stage * kStageBytes;
           mbar_arrive_expect_tx(&full_bar[stage], a_box_bytes + kBBytes);
           // A: {c, input col, input row, image} box {BK, P, R, box_n} at (c0, ow0, oh0 + fh, n0)
           asm volatile(
@@ -114,9 +126,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               "%6}], [%2];\n" ::"r"(smem_u32(st)),
               "l"(&tmap_a), "r"(smem_u32(&full_bar[stage])), "r"(c0), "r"(ow0), "r"(oh0 + fh), "r"(n0)
               : "memory");
+          if constexpr (!RB)
 #pragma unroll
-          for (int fw = 0; fw < WF; ++fw)
-            tma_load_2d(st + kABytes + fw * N * kRowBytes, &tmap_b, &full_bar[stage],
+            for (int fw = 0; fw < WF; ++fw)
+              tma_load_2d(st + kABytes + fw * N * kRowBytes, &tmap_b, &full_bar[stage],
                         (fh * WF + fw) * a.c_slabs * kBK + c0, co_blk * N);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -125,6 +138,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      if constexpr (RB) mbar_wait(&bres_bar, 0);
       for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -132,14 +146,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (uint32_t ks = 0; ks < a.k_slabs; ++ks) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          const uint32_t abase = smem_u32(smem + stage * kStageBytes);
-          const uint32_t bbase = abase + kABytes;
+          const uint32_t abase = smem_u32(stages + stage * kStageBytes);
+          const uint32_t bbase = RB ? smem_u32(smem) + ks * WF * N * kRowBytes : abase + kABytes;
 #pragma unroll
           for (int fw = 0; fw < WF; ++fw) {
 #pragma unroll
             for (int kk = 0; kk < kBK / kUK; ++kk) {
               const uint32_t aaddr = abase + fw * kRowBytes + kk * 32;
-              const uint64_t ad = BASEOFF ? smem_desc_sw128_off(aaddr) : smem_desc_sw128(aaddr);
+              const uint64_t ad = smem_desc_sw128(aaddr);
               mma<BF16>(tmem_d, ad, smem_desc_sw128(bbase + fw * N * kRowBytes + kk * 32), kIdesc,
                         (ks | fw | kk) != 0);
             }
@@ -243,7 +257,7 @@ inline double shift_tile(int64_t n, int64_t h_out, int64_t w_out, int w_f, Shift
   return static_cast<double>(a.box_w) * a.rows * a.box_n / kTileM;
 }
 
-template <bool BF16, int N, int STAGES, int WF>
+template <bool BF16, int N, int STAGES, int WF, bool RB>
 static int launch_shift(ShiftArgs a, const void* x_cl, const void* packed, int64_t c_in, int64_t h, int64_t w,
                         int64_t Mp, int64_t Kp, cudaStream_t stream, const char** err) {
   constexpr int kBK = BF16 ? 64 : 32;
@@ -282,10 +296,11 @@ static int launch_shift(ShiftArgs a, const void* x_cl, const void* packed, int64
     }
   }
   a.co_tiles = static_cast<uint32_t>(Mp / N);
-  const size_t smem = static_cast<size_t>(STAGES) * (kARows + WF * N) * kRowBytes + 1024;
+  const size_t rb = RB ? static_cast<size_t>(a.k_slabs) * WF * N * kRowBytes : 0;
+  const size_t smem = rb + static_cast<size_t>(STAGES) * (kARows + (RB ? 0 : WF * N)) * kRowBytes + 1024;
   // Measured on B200: the SW128 swizzle phase follows the absolute smem address, so the
-  // row-shifted start needs no descriptor base offset (BASEOFF=true gives wrong results).
-  auto kern = conv_tc_shift_kernel<BF16, N, STAGES, WF, false>;
+  // row-shifted start address needs no descriptor base offset.
+  auto kern = conv_tc_shift_kernel<BF16, N, STAGES, WF, RB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
@@ -352,12 +367,24 @@ int im2win_try_conv_tc_shift(const void* x_cl, const float* flt, float* out, voi
                                                              static_cast<int>(c_in), h_f, w_f, static_cast<int>(Mp),
                                                              static_cast<int>(Kc));
   int rc;
-#define IM2WIN_SH(BF, NN, ST, WFF) rc = launch_shift<BF, NN, ST, WFF>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err)
+  // Filter-resident mode: when the packed filter fits next to 4 A stages it is loaded
+  // once per CTA (one Co tile) and only window tiles stream through the ring.
+  const size_t rb_bytes = static_cast<size_t>(a.k_slabs) * w_f * N * kRowBytes;
+  const bool rb = Mp == N && rb_bytes + 4 * kARows * kRowBytes + 1024 <= 227 * 1024 &&
+                  !(getenv("IM2WIN_SHIFT_RB") && atoi(getenv("IM2WIN_SHIFT_RB")) == 0);
+#define IM2WIN_SH(BF, NN, ST, WFF, RBB) \
+  rc = launch_shift<BF, NN, ST, WFF, RBB>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err)
   if (w_f == 3) {
-    if (bf16) { if (N == 64) IM2WIN_SH(true, 64, 5, 3); else IM2WIN_SH(true, 128, 3, 3); }
-    else { if (N == 64) IM2WIN_SH(false, 64, 5, 3); else IM2WIN_SH(false, 128, 3, 3); }
+    if (bf16) {
+      if (N == 64) { if (rb) IM2WIN_SH(true, 64, 4, 3, true); else IM2WIN_SH(true, 64, 5, 3, false); }
+      else { if (rb) IM2WIN_SH(true, 128, 4, 3, true); else IM2WIN_SH(true, 128, 3, 3, false); }
+    } else {
+      if (N == 64) { if (rb) IM2WIN_SH(false, 64, 4, 3, true); else IM2WIN_SH(false, 64, 5, 3, false); }
+      else { if (rb) IM2WIN_SH(false, 128, 4, 3, true); else IM2WIN_SH(false, 128, 3, 3, false); }
+    }
   } else {
-    if (bf16) IM2WIN_SH(true, 64, 3, 5); else IM2WIN_SH(false, 64, 3, 5);
+    if (bf16) { if (rb) IM2WIN_SH(true, 64, 4, 5, true); else IM2WIN_SH(true, 64, 3, 5, false); }
+    else { if (rb) IM2WIN_SH(false, 64, 4, 5, true); else IM2WIN_SH(false, 64, 3, 5, false); }
   }
 #undef IM2WIN_SH
   return rc == 0 ? 1 : -rc;
