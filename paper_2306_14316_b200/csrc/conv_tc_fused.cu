@@ -61,6 +61,36 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restri
   }
 }
 
+// Few channels (c_pad <= 8, e.g. the RGB input layers): one thread per pixel reads its
+// C values (coalesced along the pixel axis) and writes the padded pixel with one
+// 16/32-byte store; the 32-channel smem transpose would leave most of its tile empty.
+template <bool BF16>
+__global__ void __launch_bounds__(256) nchw_to_nhwc_small_kernel(const float* __restrict__ src, void* __restrict__ dst,
+                                                                 uint32_t c_in, uint32_t c_pad, uint64_t hw,
+                                                                 uint64_t total) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t img = i / hw, p = i % hw;
+    const float* s = src + img * c_in * hw + p;
+    float v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = (static_cast<uint32_t>(c) < c_in) ? __ldg(s + c * hw) : 0.0f;
+    if constexpr (BF16) {
+      // c_pad == 8 for bf16 (16-byte pitch)
+      uint4 q;
+      q.x = pack_bf16x2(v[0], v[1]);
+      q.y = pack_bf16x2(v[2], v[3]);
+      q.z = pack_bf16x2(v[4], v[5]);
+      q.w = pack_bf16x2(v[6], v[7]);
+      reinterpret_cast<uint4*>(dst)[i] = q;
+    } else {
+      float4* d = reinterpret_cast<float4*>(dst) + i * (c_pad / 4);
+      d[0] = make_float4(v[0], v[1], v[2], v[3]);
+      if (c_pad == 8) d[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+  }
+}
+
 struct FusedArgs {
   float* __restrict__ out;
   uint32_t n_img, h_out, w_out, hw, co;
@@ -317,6 +347,22 @@ int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c
   if (total >= (1ll << 32) || hw >= (1ll << 31)) {
     *err = "nchw_to_nhwc: extents exceed the kernel's index range";
     return 1;
+  }
+  if (cp <= 8) {
+    const uint64_t pixels = static_cast<uint64_t>(n) * hw;
+    const uint32_t g = static_cast<uint32_t>(std::min<uint64_t>((pixels + 255) / 256, 148 * 32));
+    if (bf16)
+      im2win::tc::nchw_to_nhwc_small_kernel<true><<<g, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
+                                                                         static_cast<uint32_t>(cp), hw, pixels);
+    else
+      im2win::tc::nchw_to_nhwc_small_kernel<false><<<g, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
+                                                                          static_cast<uint32_t>(cp), hw, pixels);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      *err = cudaGetErrorString(e);
+      return 2;
+    }
+    return 0;
   }
   const uint32_t grid = static_cast<uint32_t>(total < 148 * 16 ? total : 148 * 16);
   if (bf16)

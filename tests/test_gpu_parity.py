@@ -237,3 +237,21 @@ def test_tc_fused_padded_channels(variant):
         ref = orc.conv_direct(inp, flt, s)
         out = pkg.conv_im2win_opt(inp, flt, params, variant=variant).numpy()
         assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (c, hf, s)
+
+
+@pytest.mark.slow
+def test_64bit_indexing_conv4_n256():
+    """at N=256, conv4's Ĩ has 2.79e9 > 2^31 elements.  Sampled images at the
+    far end of the batch must still be bit-exact (64-bit offsets in transform and conv)."""
+    cfg = replace(BENCHMARKS["conv4"], batch=256, seed=13)
+    g = torch.Generator(device="cpu").manual_seed(13)
+    flt = torch.randn((cfg.c_out, cfg.c_in, cfg.h_f, cfg.w_f), generator=g)
+    x = torch.randn((cfg.batch, cfg.c_in, cfg.h_in, cfg.w_in), generator=g)
+    win = pkg.im2win(x.to(DEV), cfg.params)
+    assert win.elements() > 2 ** 31
+    out = pkg.compute_from_windows_opt(win, flt.to(DEV), cfg.params)
+    for i in (0, 200, 255):
+        ref_w = orc.im2win_fill(x[i:i + 1].numpy(), cfg.h_f, cfg.w_f, cfg.stride)
+        assert bits_equal(win.data[i:i + 1].cpu().numpy(), ref_w), i
+        ref = orc.conv_direct(x[i:i + 1].numpy(), flt.numpy(), cfg.stride)
+        assert bits_equal(out.data[i:i + 1].cpu().numpy(), ref), i
