@@ -11,6 +11,9 @@
 //     (each input row feeds ceil(Hf/s) output rows, so HBM reads it once);
 //   * the output range is written with aligned 16-byte stores, the (c, u)
 //     decode of each element stepped incrementally from one fast division.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace im2win {
@@ -103,6 +106,174 @@ __global__ void __launch_bounds__(256) im2win_transform_kernel(const TransformAr
   for (uint32_t v = threadIdx.x; v < nvec; v += blockDim.x) __stcs(d4 + v, o4[v]);
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined persistent variant (the production path).
+//
+// Same chunking as above (a chunk = R consecutive output rows = one contiguous
+// output range; its input rows = one contiguous input range), but each CTA
+// walks chunks blockIdx.x, +gridDim.x, ... with two shared-memory stages:
+//   * the input range of chunk j+1 is fetched by one TMA bulk copy
+//     (cp.async.bulk, mbarrier complete_tx) while chunk j is being built;
+//   * the built output range of chunk j leaves by one TMA bulk store
+//     (cp.async.bulk.global.shared::cta, bulk_group) that drains while chunk
+//     j+1 is built; its buffer is reused two chunks later after
+//     cp.async.bulk.wait_group.read.
+// Unaligned input/output ends (< 16 B) are moved with plain loads/stores.
+// Needs 16 B aligned src/dst base pointers (checked by the launcher).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kXformThreads = 256;
+
+struct PipeArgs {
+  TransformArgs t;
+  uint64_t src_floats;   // total input elements (bulk loads never read past it)
+  uint32_t n_chunks;
+  uint32_t obuf_floats;  // per stage, multiple of 4
+  uint32_t rowoff_ints;  // per stage, multiple of 4
+};
+
+IM2WIN_DEVICE void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+IM2WIN_DEVICE void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+IM2WIN_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N>
+IM2WIN_DEVICE void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+IM2WIN_DEVICE void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
+struct ChunkGeom {
+  uint32_t g0, nrows;
+  uint64_t r_lo, f_begin, f_end, a_begin, a_end;
+};
+
+IM2WIN_DEVICE ChunkGeom chunk_geom(const PipeArgs& p, uint32_t chunk) {
+  const TransformArgs& a = p.t;
+  ChunkGeom c;
+  c.g0 = chunk * a.rows_per_cta;
+  c.nrows = min(a.rows_per_cta, a.rows_total - c.g0);
+  c.r_lo = in_row_of(a, c.g0);
+  const uint64_t r_hi = in_row_of(a, c.g0 + c.nrows - 1) + a.h_f;
+  c.f_begin = c.r_lo * a.w_in;
+  c.f_end = r_hi * a.w_in;
+  c.a_begin = c.f_begin & ~3ull;
+  c.a_end = min((c.f_end + 3) & ~3ull, p.src_floats & ~3ull);
+  return c;
+}
+
+// Build one output chunk in shared memory.  Items (row gl, column col) are
+// strided by the CTA size; (gl, col) advances incrementally (no division in
+// the loop).  HF > 0 unrolls the Hf copies (loads first, then stores).
+template <int HF>
+IM2WIN_DEVICE void build_chunk(const TransformArgs& a, const float* __restrict__ tb, const int* __restrict__ ro,
+                               float* __restrict__ ob, uint32_t nrows, uint32_t tid, uint32_t dg, uint32_t dc) {
+  const uint32_t w_eff = a.w_eff, w_in = a.w_in, row_len = a.row_len;
+  const uint32_t items = nrows * w_eff;
+  uint32_t gl, col;
+  a.fd_weff.divmod(tid, gl, col);
+  for (uint32_t it = tid; it < items; it += kXformThreads) {
+    const float* tp = tb + ro[gl] + col;
+    if constexpr (HF > 0) {
+      float* op = ob + gl * row_len + col * HF;
+      float v[HF];
+#pragma unroll
+      for (int u = 0; u < HF; ++u) v[u] = tp[u * w_in];
+#pragma unroll
+      for (int u = 0; u < HF; ++u) op[u] = v[u];
+    } else {
+      const uint32_t hf = a.h_f;
+      float* op = ob + gl * row_len + col * hf;
+      for (uint32_t u = 0; u < hf; ++u) op[u] = tp[u * w_in];
+    }
+    col += dc;
+    gl += dg;
+    if (col >= w_eff) {
+      col -= w_eff;
+      ++gl;
+    }
+  }
+}
+
+template <int HF>
+__global__ void __launch_bounds__(kXformThreads) im2win_transform_pipe_kernel(const PipeArgs p) {
+  const TransformArgs& a = p.t;
+  uint32_t dg, dc;  // kXformThreads = dg * w_eff + dc
+  a.fd_weff.divmod(kXformThreads, dg, dc);
+  extern __shared__ __align__(16) float smem[];
+  __shared__ __align__(8) uint64_t full[2];
+  int* rowoff = reinterpret_cast<int*>(smem);          // [2][rowoff_ints]
+  float* tile = smem + 2 * p.rowoff_ints;               // [2][tile_floats]
+  float* obuf = tile + 2 * a.tile_floats;               // [2][obuf_floats]
+  const uint32_t tid = threadIdx.x;
+
+  if (tid == 0) {
+    mbarrier_init(&full[0], 1);
+    mbarrier_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](uint32_t chunk, int b) {
+    const ChunkGeom c = chunk_geom(p, chunk);
+    const uint32_t bytes = c.a_end > c.a_begin ? static_cast<uint32_t>(c.a_end - c.a_begin) * 4u : 0u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&full[b])), "r"(bytes)
+                 : "memory");
+    if (bytes) bulk_load(tile + b * a.tile_floats, a.src + c.a_begin, bytes, &full[b]);
+  };
+
+  uint32_t chunk = blockIdx.x;
+  if (tid == 0 && chunk < p.n_chunks) issue(chunk, 0);
+  for (uint32_t j = 0; chunk < p.n_chunks; chunk += gridDim.x, ++j) {
+    const int b = j & 1;
+    const uint32_t next = chunk + gridDim.x;
+    // stage b^1 was last read by chunk j-1's build, which ended at a CTA barrier
+    if (tid == 0 && next < p.n_chunks) issue(next, b ^ 1);
+
+    const ChunkGeom c = chunk_geom(p, chunk);
+    float* tb = tile + b * a.tile_floats;
+    float* ob = obuf + b * p.obuf_floats;
+    int* ro = rowoff + b * p.rowoff_ints;
+    const uint32_t tshift = static_cast<uint32_t>(c.f_begin - c.a_begin);
+    for (uint32_t gl = tid; gl < c.nrows; gl += blockDim.x)
+      ro[gl] = static_cast<int>((in_row_of(a, c.g0 + gl) - c.r_lo) * a.w_in + tshift);
+
+    mbarrier_wait_parity(&full[b], (j >> 1) & 1);
+    // input tail the bulk copy could not cover (end of the tensor, < 4 floats)
+    for (uint64_t f = max(c.a_end, c.a_begin) + tid; f < c.f_end; f += blockDim.x)
+      tb[f - c.a_begin] = a.src[f];
+    // the bulk store of chunk j-2 read this stage's obuf; keep only chunk j-1's in flight
+    if (tid == 0) bulk_wait_read<1>();
+    __syncthreads();
+
+    // build: item = (row gl, column col) writes Hf values (conflict-free, see above)
+    const uint64_t e_begin = static_cast<uint64_t>(c.g0) * a.row_len;
+    const uint32_t count = c.nrows * a.row_len;
+    const uint32_t head = min(count, static_cast<uint32_t>((4u - (e_begin & 3u)) & 3u));
+    const uint32_t oshift = (4u - head) & 3u;
+    build_chunk<HF>(a, tb, ro, ob + oshift, c.nrows, tid, dg, dc);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+
+    float* dst = a.dst + e_begin;
+    const uint32_t nvec = (count - head) >> 2;
+    const uint32_t tail = head + (nvec << 2);
+    if (tid < head) dst[tid] = ob[oshift + tid];
+    if (tail + tid < count) dst[tail + tid] = ob[oshift + tail + tid];
+    if (tid == 0) {
+      if (nvec) bulk_store(dst + head, ob + oshift + head, nvec * 16u);
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
 // Host planning: rows per CTA and the worst-case input-row span.
 struct TransformPlan {
   uint32_t rows_per_cta;
@@ -128,9 +299,10 @@ static uint32_t host_span(uint32_t R, uint32_t h_out, uint32_t h_in, uint32_t s,
 }
 
 static TransformPlan plan_transform(uint32_t rows_total, uint32_t h_out, uint32_t h_in, uint32_t w_in,
-                                    uint32_t s, uint32_t h_f, uint32_t row_len, size_t smem_cap) {
+                                    uint32_t s, uint32_t h_f, uint32_t row_len, size_t smem_cap,
+                                    uint32_t target_floats = 8192) {
   TransformPlan p{};
-  uint32_t R = (8192 + row_len - 1) / row_len;
+  uint32_t R = (target_floats + row_len - 1) / row_len;
   uint32_t min_r = (2 * h_f + s - 1) / s;
   if (R < min_r) R = min_r;
   if (R > rows_total) R = rows_total;
@@ -187,11 +359,59 @@ int im2win_launch_transform(const float* src, float* dst, int64_t n, int64_t c, 
   a.fd_hf = FastDiv(a.h_f);
   a.fd_weff = FastDiv(a.w_eff);
   (void)w_f;
-  if (p.smem_bytes > 48 * 1024) {
-    cudaFuncSetAttribute(im2win_transform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem_cap));
+  const bool aligned = (reinterpret_cast<uintptr_t>(src) & 15u) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
+  // pipelined path: two stages of (row offsets, staged input, output chunk)
+  const char* tgt_env = getenv("IM2WIN_XFORM_CHUNK");
+  const uint32_t target = tgt_env ? static_cast<uint32_t>(atoi(tgt_env)) : 4096u;
+  TransformPlan q = plan_transform(static_cast<uint32_t>(rows_total), static_cast<uint32_t>(h_out),
+                                   static_cast<uint32_t>(h), static_cast<uint32_t>(w), static_cast<uint32_t>(stride),
+                                   static_cast<uint32_t>(h_f), static_cast<uint32_t>(row_len), 48 * 1024, target);
+  PipeArgs pa;
+  pa.t = a;
+  pa.t.rows_per_cta = q.rows_per_cta;
+  pa.t.tile_floats = (q.span * static_cast<uint32_t>(w) + 4 + 3) & ~3u;
+  pa.obuf_floats = (q.rows_per_cta * static_cast<uint32_t>(row_len) + 4 + 3) & ~3u;
+  pa.rowoff_ints = (q.rows_per_cta + 3) & ~3u;
+  pa.src_floats = static_cast<uint64_t>(n * c * h * w);
+  pa.n_chunks = q.grid;
+  const size_t pipe_smem = 2ull * (pa.rowoff_ints + pa.t.tile_floats + pa.obuf_floats) * 4;
+  if (aligned && pipe_smem <= 200 * 1024) {
+    void (*kern)(const PipeArgs) = im2win_transform_pipe_kernel<0>;
+    int ki = 0;
+    switch (h_f) {
+      case 3: kern = im2win_transform_pipe_kernel<3>; ki = 1; break;
+      case 5: kern = im2win_transform_pipe_kernel<5>; ki = 2; break;
+      case 7: kern = im2win_transform_pipe_kernel<7>; ki = 3; break;
+      case 11: kern = im2win_transform_pipe_kernel<11>; ki = 4; break;
+      default: break;
+    }
+    // per-(kernel, smem size) occupancy cache: keeps host work per call small
+    static thread_local struct { int dev, ki; size_t smem; int occ; int sms; } cache[8];
+    static thread_local int cache_n = 0;
+    int occ = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    for (int i = 0; i < cache_n; ++i)
+      if (cache[i].dev == dev && cache[i].ki == ki && cache[i].smem == pipe_smem) {
+        occ = cache[i].occ;
+        sms = cache[i].sms;
+      }
+    if (!occ) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kXformThreads, pipe_smem);
+      if (occ < 1) occ = 1;
+      cache[cache_n < 8 ? cache_n : 7] = {dev, ki, pipe_smem, occ, sms};
+      if (cache_n < 8) ++cache_n;
+    }
+    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(pa.n_chunks, static_cast<uint64_t>(sms) * occ));
+    kern<<<grid, kXformThreads, pipe_smem, stream>>>(pa);
+  } else {
+    if (p.smem_bytes > 48 * 1024) {
+      cudaFuncSetAttribute(im2win_transform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem_cap));
+    }
+    im2win_transform_kernel<<<p.grid, 256, p.smem_bytes, stream>>>(a);
   }
-  im2win_transform_kernel<<<p.grid, 256, p.smem_bytes, stream>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
