@@ -44,6 +44,29 @@ def load_peaks() -> dict:
     return dict(PEAKS_FALLBACK)
 
 
+def load_traffic(names, batch: int, variant: str):
+    """DRAM traffic of the step's kernels from the committed ncu --set full capture.
+
+    profiles/r01_traffic_n128.json is written by tools/ncu_traffic.py from one
+    `ncu --set full` capture per layer (dram__bytes_read.sum + dram__bytes_write.sum).
+    Returns None when it does not cover this workload.
+    """
+    p = ROOT / "profiles" / "r01_traffic_n128.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    if d.get("batch") != batch or d.get("variant") != variant or not all(n in d["layers"] for n in names):
+        return None
+    conv = [d["layers"][n]["conv_dram_bytes"] for n in names]
+    xf = [d["layers"][n]["transform_dram_bytes"] for n in names]
+    alg = [d["layers"][n]["conv_algorithmic_bytes"] for n in names]
+    return {"source": str(p.relative_to(ROOT)), "capture": d.get("capture"),
+            "conv_bytes_per_launch": sum(conv) / len(conv),
+            "conv_algorithmic_bytes_per_launch": sum(alg) / len(alg),
+            "transform_bytes_per_launch": sum(xf) / len(xf),
+            "per_layer": {n: d["layers"][n] for n in names}}
+
+
 # ---------------------------------------------------------------------------
 # reference arm: CPU oracle on the host cores
 # ---------------------------------------------------------------------------
@@ -228,6 +251,12 @@ def main() -> None:
     torch.cuda.synchronize(dev)
 
     # ---- timed region: exactly K steps ----
+    # Events around every transform and conv launch are recorded inside the timed
+    # region (same stream, GPU kept busy by the queue) so the dominant kernel's
+    # average launch duration comes from the run that produces `value`.
+    n_l = len(layers)
+    marks = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n_l)]
+             for _ in range(args.steps)]
     sampler = ClockSampler(dev.index)
     sampler.start()
     time.sleep(0.3)
@@ -236,8 +265,13 @@ def main() -> None:
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for _ in range(args.steps):
-        step()
+    for k in range(args.steps):
+        for L, m in zip(layers, marks[k]):
+            m[0].record(stream)
+            im2win_into(L["x"], L["win"], L["cfg"].params)
+            m[1].record(stream)
+            conv_windows_into(L["win"], L["f"], L["out"], L["cfg"].params, L["cfg"].w_eff, None, args.variant)
+            m[2].record(stream)
     ev1.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
@@ -247,32 +281,23 @@ def main() -> None:
     value = flops_step * world * args.steps / (elapsed_ms * 1e-3) / 1e12
     ms_per_step = elapsed_ms / args.steps
 
-    # ---- per-layer breakdown (events around each kernel, best of 3) ----
+    # ---- per-layer breakdown from the timed region (mean over the K steps) ----
     per_layer = []
     conv_ms_total = 0.0
     tr_ms_total = 0.0
-    for L in layers:
+    for li, L in enumerate(layers):
         cfg = L["cfg"]
-        best_t, best_c = 1e30, 1e30
-        for _ in range(3):
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            e[0].record(stream)
-            im2win_into(L["x"], L["win"], cfg.params)
-            e[1].record(stream)
-            conv_windows_into(L["win"], L["f"], L["out"], cfg.params, cfg.w_eff, None, args.variant)
-            e[2].record(stream)
-            torch.cuda.synchronize(dev)
-            best_t = min(best_t, e[0].elapsed_time(e[1]))
-            best_c = min(best_c, e[1].elapsed_time(e[2]))
-        conv_ms_total += best_c
-        tr_ms_total += best_t
+        t_tr = statistics.fmean(marks[k][li][0].elapsed_time(marks[k][li][1]) for k in range(args.steps))
+        t_cv = statistics.fmean(marks[k][li][1].elapsed_time(marks[k][li][2]) for k in range(args.steps))
+        conv_ms_total += t_cv
+        tr_ms_total += t_tr
         tb = cfg.transform_bytes()
         per_layer.append({
             "name": cfg.name, "batch": cfg.batch, "gflop": cfg.flops / 1e9,
-            "transform_ms": best_t, "conv_ms": best_c,
-            "tflops": cfg.flops / ((best_t + best_c) * 1e-3) / 1e12,
-            "tflops_conv_only": cfg.flops / (best_c * 1e-3) / 1e12,
-            "transform_gbs": tb / (best_t * 1e-3) / 1e9,
+            "transform_ms": t_tr, "conv_ms": t_cv,
+            "tflops": cfg.flops / ((t_tr + t_cv) * 1e-3) / 1e12,
+            "tflops_conv_only": cfg.flops / (t_cv * 1e-3) / 1e12,
+            "transform_gbs": tb / (t_tr * 1e-3) / 1e9,
             "footprint_bytes": {"raw": 4 * cfg.elems("raw"), "im2col": 4 * cfg.elems("im2col"),
                                 "im2win": 4 * cfg.elems("im2win")},
         })
@@ -293,18 +318,28 @@ def main() -> None:
 
     conv_flops = flops_step
     achieved = conv_flops / (conv_ms_total * 1e-3) / 1e12
+    traffic = load_traffic(names, args.batch, args.variant)
     pk = peak["exact"] if args.variant == "fp32-exact" else peak["ffma"]
     roofline = {"bound": "fp32-simt", "kernel": "conv_simt_kernel (FMUL+FADD)" if args.variant == "fp32-exact" else args.variant,
                 "achieved": achieved, "peak": pk, "unit": "TFLOP/s", "frac": achieved / pk,
                 "peak_source": "measured on this box in this run by im2win_bench_fp32_peak "
                                f"({'FMUL+FADD' if args.variant == 'fp32-exact' else 'FFMA'} chains, 148x8 CTAs)",
-                "peak_ffma": peak["ffma"], "traffic": None,
+                "peak_ffma": peak["ffma"], "traffic": traffic and traffic["conv_bytes_per_launch"],
+                "traffic_detail": traffic,
+                "launches_per_step": {"conv": len(layers), "transform": len(layers), "pack_filter": len(layers)},
+                "achieved_note": "sum of algorithmic FLOPs of the step's conv launches / sum of their mean "
+                                 "durations (CUDA events around each launch inside the timed region)",
                 "transform": {"bound": "hbm", "achieved": sum(L["cfg"].transform_bytes() for L in layers) / (tr_ms_total * 1e-3) / 1e9,
-                              "peak": peaks["hbm_gbs"], "unit": "GB/s", "peak_source": peaks["source"]}}
+                              "peak": peaks["hbm_gbs"], "unit": "GB/s", "peak_source": peaks["source"],
+                              "traffic": traffic and traffic["transform_bytes_per_launch"],
+                              "algorithmic_bytes_per_launch": sum(L["cfg"].transform_bytes() for L in layers) / len(layers)}}
     roofline["transform"]["frac"] = roofline["transform"]["achieved"] / roofline["transform"]["peak"]
     roofline["conv_share_of_step"] = conv_ms_total / (conv_ms_total + tr_ms_total)
 
-    # ---- e2e: public API, pinned host inputs -> device -> result back to host ----
+    # ---- e2e: public host API (numpy-style call: host operands in, host result out) ----
+    # conv_im2win_opt_host streams each layer's batch in chunks (upload / transform+conv /
+    # download overlapped on three streams, csrc/pipeline.cu); every byte crosses PCIe inside
+    # the timed region.
     e2e = None
     host = []
     for L in layers:
@@ -315,10 +350,7 @@ def main() -> None:
 
     def e2e_step():
         for L, h in zip(layers, host):
-            x = h["x"].to(dev, non_blocking=True)
-            f = h["f"].to(dev, non_blocking=True)
-            y = pkg.conv_im2win_opt(x, f, L["cfg"].params, variant=args.variant)
-            h["out"].copy_(y.data, non_blocking=True)
+            pkg.conv_im2win_opt_host(h["x"], h["f"], L["cfg"].params, variant=args.variant, out=h["out"])
 
     e2e_step()
     torch.cuda.synchronize(dev)
@@ -330,9 +362,14 @@ def main() -> None:
     e1.record(stream)
     torch.cuda.synchronize(dev)
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.e2e_steps
+    # the streamed result must be the device path's result (bitwise), checked once outside the timing
+    e2e_ok = all(torch.equal(h["out"].view(torch.int32), L["out"].cpu().view(torch.int32))
+                 for L, h in zip(layers, host)) if args.variant == "fp32-exact" else None
     e2e = {"value": flops_step * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOPS",
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-           "path": "paper_2306_14316_b200.conv_im2win_opt (C ABI) with pinned host operands"}
+           "path": "paper_2306_14316_b200.conv_im2win_opt_host -> im2win_conv_host_f32 (C ABI), pinned host "
+                   "operands, chunked upload/compute/download overlap",
+           "bitwise_equal_to_device_path": e2e_ok}
     del host
 
     # ---- baselines on the same B200 (rank 0): cuDNN and im2col+cuBLAS, FP32 (TF32 off) ----
@@ -481,7 +518,7 @@ def main() -> None:
         "roofline": roofline,
         "cpu_baseline": cpu_baseline,
         "e2e": e2e,
-        "gpu_launches": 3 * n_layers * args.steps,
+        "gpu_launches": 3 * n_layers * args.steps,  # transform + pack_filter + conv per layer per step
         "clocks": clocks,
         "layers": per_layer,
         "baselines": baselines,

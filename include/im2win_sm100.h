@@ -113,6 +113,26 @@ int im2win_conv_fused(const void* x_nhwc, const float* flt, float* out, int64_t 
                       int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
                       int32_t variant, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Host-buffer entry point (extension of conv_im2win_opt, optimized.py:237-241) ----
+ * The reference is called with host (numpy) operands and returns a host array.
+ * This runs transform + conv over host buffers: the batch is cut into chunks of
+ * chunk_images (<= 0: about n/8) and a three-stream pipeline overlaps the
+ * upload of chunk k+1, the kernels of chunk k and the download of chunk k-1.
+ * host_in (n,c_in,h,w), host_flt (c_out,c_in,h_f,w_f), host_out (n,c_out,h_out,w_out)
+ * are host memory (page-locked for overlap); workspace is device memory of at
+ * least im2win_conv_host_workspace_bytes(...) bytes on the device to run on.
+ * Ordered after prior work on `stream`; blocks until host_out is written.
+ * Results are bit-identical to im2win_transform_f32 + im2win_conv_f32
+ * (FP32 variants) or im2win_nchw_to_nhwc + im2win_conv_fused (TF32/BF16). */
+size_t im2win_conv_host_workspace_bytes(int64_t n, int64_t c_in, int64_t h, int64_t w, int64_t c_out,
+                                        int32_t h_f, int32_t w_f, int32_t stride, int32_t variant,
+                                        int64_t chunk_images);
+
+int im2win_conv_host_f32(const float* host_in, const float* host_flt, float* host_out, int64_t n,
+                         int64_t c_in, int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f,
+                         int32_t stride, const im2win_tile_plan* plan, int32_t variant,
+                         int64_t chunk_images, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Measurement utility (bench.py only): launches `blocks` x 256 threads that each
  * retire 2*32*iters flops of independent FP32 multiply-add chains; exact != 0
  * issues FMUL+FADD (the conv's bit-exact pair), else FFMA.  Used to measure the

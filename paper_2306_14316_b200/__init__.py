@@ -21,7 +21,13 @@ from .errors import (
 from .tensors import ConvParams, Tensor4, check_conv_operands, max_rel_diff, normalized_max_diff, output_dims
 from .plan import GemmDims, TilePlan, compose_k, compose_n, decompose_k, decompose_n, default_plan, gpu_plan
 from .layouts import Im2winTensor, effective_width, footprint_elems, im2win, im2win_gather
-from .kernels import compute_from_windows_basic, compute_from_windows_opt, conv_im2win_basic, conv_im2win_opt
+from .kernels import (
+    compute_from_windows_basic,
+    compute_from_windows_opt,
+    conv_im2win_basic,
+    conv_im2win_opt,
+    conv_im2win_opt_host,
+)
 from .workloads import BENCHMARKS, BenchConfig, make_inputs
 from .fixture_io import read_tensor, write_tensor
 
@@ -52,6 +58,7 @@ __all__ = [
     "compute_from_windows_opt",
     "conv_im2win_basic",
     "conv_im2win_opt",
+    "conv_im2win_opt_host",
     "decompose_k",
     "decompose_n",
     "default_plan",

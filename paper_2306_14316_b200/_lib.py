@@ -37,6 +37,8 @@ EXPORTED_SYMBOLS = (
     "im2win_conv_fused_workspace_bytes",
     "im2win_conv_fused",
     "im2win_conv_basic_f32",
+    "im2win_conv_host_workspace_bytes",
+    "im2win_conv_host_f32",
 )
 
 
@@ -94,6 +96,11 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         lib.im2win_conv_fused.restype = ctypes.c_int
         lib.im2win_conv_basic_f32.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i32, i32, i32, vp]
         lib.im2win_conv_basic_f32.restype = ctypes.c_int
+        lib.im2win_conv_host_workspace_bytes.argtypes = [i64, i64, i64, i64, i64, i32, i32, i32, i32, i64]
+        lib.im2win_conv_host_workspace_bytes.restype = sz
+        lib.im2win_conv_host_f32.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32,
+                                             ctypes.POINTER(TilePlanC), i32, i64, vp, sz, vp]
+        lib.im2win_conv_host_f32.restype = ctypes.c_int
         if path is None:
             _lib = lib
         return lib

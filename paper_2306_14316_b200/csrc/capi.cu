@@ -49,6 +49,8 @@ static int bind_device_of(const void* ptr) {
   return 0;
 }
 
+int im2win_set_error(int code, const char* msg) { return fail(code, msg); }
+
 extern "C" {
 
 const char* im2win_last_error(void) { return g_last_error; }

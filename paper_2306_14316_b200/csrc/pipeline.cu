@@ -1,0 +1,220 @@
+// Host-buffer entry point: the whole reference call (numpy in -> numpy out,
+// winconv conv_im2win_opt, /root/reference/pkg/src/winconv/kernels/optimized.py:237-241)
+// with the host<->device copies overlapped against the kernels.
+//
+// Images are independent (reference.py:78-90), so the batch is cut into chunks
+// of `chunk` images and run as a three-stream software pipeline per device:
+//
+//   h2d  : copy input chunk k            -> in[k%2]        (waits xf[k-2])
+//   comp : transform in[k%2] -> Ĩ,  conv Ĩ -> out[k%2]      (waits h2d[k], d2h[k-2])
+//   d2h  : copy out[k%2]                  -> host output   (waits conv[k])
+//
+// so PCIe upload, compute and PCIe download of consecutive chunks run at the
+// same time (two copy engines + the SMs).  The per-chunk kernels are the same
+// C-ABI entry points a device caller uses (im2win_transform_f32 +
+// im2win_conv_f32 for the FP32 variants; im2win_nchw_to_nhwc +
+// im2win_conv_fused for TF32/BF16), so results are bit-identical to the
+// device path.  Host buffers should be page-locked for the copies to overlap;
+// pageable buffers work but serialise.  The call blocks until the output is
+// on the host.  The caller provides the device workspace
+// (im2win_conv_host_workspace_bytes); the library allocates nothing.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "../../include/im2win_sm100.h"
+
+// capi.cu: stores the message returned by im2win_last_error()
+int im2win_set_error(int code, const char* msg);
+
+namespace {
+
+constexpr int kMaxDev = 64;
+constexpr int kDepth = 2;  // input / output chunk buffers in flight
+
+struct DevPipe {
+  bool ready = false;
+  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  cudaEvent_t start = nullptr;
+  cudaEvent_t in_ready[kDepth], xf_done[kDepth], conv_done[kDepth], out_done[kDepth];
+  std::mutex mu;
+};
+
+DevPipe g_pipes[kMaxDev];
+
+struct Geometry {
+  int64_t n, c_in, h, w, c_out, h_out, w_out, w_eff;
+  int h_f, w_f, stride;
+  bool tc;
+  int64_t pitch;  // channels-last pitch for the TC path
+  size_t in_elems, mid_bytes, out_elems, flt_elems, conv_ws;
+};
+
+size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+Geometry geometry(int64_t n_chunk, int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride,
+                  int variant) {
+  Geometry g{};
+  g.n = n_chunk;
+  g.c_in = c_in;
+  g.h = h;
+  g.w = w;
+  g.c_out = c_out;
+  g.h_f = h_f;
+  g.w_f = w_f;
+  g.stride = stride;
+  g.h_out = (h - h_f) / stride + 1;
+  g.w_out = (w - w_f) / stride + 1;
+  g.w_eff = (g.w_out - 1) * stride + w_f;
+  g.tc = variant == IM2WIN_TF32 || variant == IM2WIN_BF16;
+  const int q = variant == IM2WIN_BF16 ? 8 : 4;
+  g.pitch = (c_in + q - 1) / q * q;
+  g.in_elems = static_cast<size_t>(n_chunk * c_in * h * w);
+  g.out_elems = static_cast<size_t>(n_chunk * c_out * g.h_out * g.w_out);
+  g.flt_elems = static_cast<size_t>(c_out * c_in * h_f * w_f);
+  if (g.tc) {
+    g.mid_bytes = static_cast<size_t>(n_chunk * h * w * g.pitch) * (variant == IM2WIN_BF16 ? 2 : 4);
+    g.conv_ws = im2win_conv_fused_workspace_bytes(c_in, c_out, h_f, w_f);
+  } else {
+    g.mid_bytes = static_cast<size_t>(n_chunk * c_in * g.h_out * h_f * g.w_eff) * 4;
+    g.conv_ws = im2win_conv_workspace_bytes(c_in, c_out, h_f, w_f, variant);
+  }
+  return g;
+}
+
+size_t workspace_bytes(const Geometry& g) {
+  return align_up(g.flt_elems * 4) + align_up(g.conv_ws) + align_up(g.mid_bytes) +
+         kDepth * (align_up(g.in_elems * 4) + align_up(g.out_elems * 4));
+}
+
+int64_t pick_chunk(int64_t n, int64_t chunk) {
+  if (chunk > 0) return std::min(chunk, n);
+  // ~8 chunks per call: fill/drain costs ~1/8 of the copy time, chunks stay large
+  return std::max<int64_t>(1, (n + 7) / 8);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t im2win_conv_host_workspace_bytes(int64_t n, int64_t c_in, int64_t h, int64_t w, int64_t c_out, int32_t h_f,
+                                        int32_t w_f, int32_t stride, int32_t variant, int64_t chunk_images) {
+  if (n < 1 || c_in < 1 || h < 1 || w < 1 || c_out < 1 || h_f < 1 || w_f < 1 || stride < 1 || h_f > h || w_f > w)
+    return 0;
+  const int64_t cn = pick_chunk(n, chunk_images);
+  return workspace_bytes(geometry(cn, c_in, h, w, c_out, h_f, w_f, stride, variant));
+}
+
+int im2win_conv_host_f32(const float* host_in, const float* host_flt, float* host_out, int64_t n, int64_t c_in,
+                         int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
+                         const im2win_tile_plan* plan, int32_t variant, int64_t chunk_images, void* workspace,
+                         size_t ws_bytes, void* stream) {
+  if (!host_in || !host_flt || !host_out || !workspace) return im2win_set_error(1, "im2win_conv_host_f32: null pointer");
+  if (n < 1 || c_in < 1 || h < 1 || w < 1 || c_out < 1 || h_f < 1 || w_f < 1 || stride < 1)
+    return im2win_set_error(1, "im2win_conv_host_f32: extents must be positive");
+  if (h_f > h || w_f > w) return im2win_set_error(1, "im2win_conv_host_f32: filter larger than input");
+  if (variant < IM2WIN_FP32_EXACT || variant > IM2WIN_BF16)
+    return im2win_set_error(1, "im2win_conv_host_f32: unknown variant");
+  const int64_t cn = pick_chunk(n, chunk_images);
+  const Geometry g = geometry(cn, c_in, h, w, c_out, h_f, w_f, stride, variant);
+  if (ws_bytes < workspace_bytes(g)) return im2win_set_error(1, "im2win_conv_host_f32: workspace too small");
+
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, workspace) != cudaSuccess || attr.type != cudaMemoryTypeDevice)
+    return im2win_set_error(1, "im2win_conv_host_f32: workspace is not device memory");
+  const int dev = attr.device;
+  if (dev < 0 || dev >= kMaxDev) return im2win_set_error(1, "im2win_conv_host_f32: device index out of range");
+  cudaSetDevice(dev);
+  DevPipe& P = g_pipes[dev];
+  std::lock_guard<std::mutex> lock(P.mu);
+  if (!P.ready) {
+    cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&P.comp, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&P.start, cudaEventDisableTiming);
+    for (int i = 0; i < kDepth; ++i) {
+      cudaEventCreateWithFlags(&P.in_ready[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&P.xf_done[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&P.conv_done[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&P.out_done[i], cudaEventDisableTiming);
+    }
+    if (cudaGetLastError() != cudaSuccess) return im2win_set_error(2, "im2win_conv_host_f32: stream setup failed");
+    P.ready = true;
+  }
+
+  // carve the workspace
+  char* base = static_cast<char*>(workspace);
+  float* d_flt = reinterpret_cast<float*>(base);
+  base += align_up(g.flt_elems * 4);
+  void* conv_ws = base;
+  base += align_up(g.conv_ws);
+  void* mid = base;
+  base += align_up(g.mid_bytes);
+  float* d_in[kDepth];
+  float* d_out[kDepth];
+  for (int i = 0; i < kDepth; ++i) {
+    d_in[i] = reinterpret_cast<float*>(base);
+    base += align_up(g.in_elems * 4);
+    d_out[i] = reinterpret_cast<float*>(base);
+    base += align_up(g.out_elems * 4);
+  }
+
+  // everything is ordered after the caller's prior work on `stream` (it may own the workspace)
+  cudaStream_t user = static_cast<cudaStream_t>(stream);
+  cudaEventRecord(P.start, user);
+  cudaStreamWaitEvent(P.h2d, P.start, 0);
+  cudaStreamWaitEvent(P.comp, P.start, 0);
+  cudaStreamWaitEvent(P.d2h, P.start, 0);
+  cudaMemcpyAsync(d_flt, host_flt, g.flt_elems * 4, cudaMemcpyHostToDevice, P.comp);
+
+  const int64_t img_in = c_in * h * w;
+  const int64_t img_out = c_out * g.h_out * g.w_out;
+  const int64_t n_chunks = (n + cn - 1) / cn;
+  int rc = 0;
+  for (int64_t k = 0; k < n_chunks && rc == 0; ++k) {
+    const int s = static_cast<int>(k % kDepth);
+    const int64_t i0 = k * cn;
+    const int64_t nk = std::min(cn, n - i0);
+    // upload (buffer s was last read by chunk k-2's transform)
+    if (k >= kDepth) cudaStreamWaitEvent(P.h2d, P.xf_done[s], 0);
+    cudaMemcpyAsync(d_in[s], host_in + i0 * img_in, static_cast<size_t>(nk * img_in) * 4, cudaMemcpyHostToDevice,
+                    P.h2d);
+    cudaEventRecord(P.in_ready[s], P.h2d);
+    // compute (output buffer s was last read by chunk k-2's download)
+    cudaStreamWaitEvent(P.comp, P.in_ready[s], 0);
+    if (k >= kDepth) cudaStreamWaitEvent(P.comp, P.out_done[s], 0);
+    if (g.tc) {
+      rc = im2win_nchw_to_nhwc(d_in[s], mid, nk, c_in, h, w, variant == IM2WIN_BF16 ? 1 : 0, P.comp);
+      cudaEventRecord(P.xf_done[s], P.comp);
+      if (!rc)
+        rc = im2win_conv_fused(mid, d_flt, d_out[s], nk, c_in, h, w, c_out, h_f, w_f, stride, variant, conv_ws,
+                               g.conv_ws, P.comp);
+    } else {
+      rc = im2win_transform_f32(d_in[s], static_cast<float*>(mid), nk, c_in, h, w, h_f, w_f, stride, P.comp);
+      cudaEventRecord(P.xf_done[s], P.comp);
+      if (!rc)
+        rc = im2win_conv_f32(static_cast<float*>(mid), d_flt, d_out[s], nk, c_in, c_out, g.h_out, g.w_out,
+                             static_cast<int64_t>(h_f) * g.w_eff, h_f, w_f, stride, plan, variant, conv_ws, g.conv_ws,
+                             P.comp);
+    }
+    cudaEventRecord(P.conv_done[s], P.comp);
+    // download
+    cudaStreamWaitEvent(P.d2h, P.conv_done[s], 0);
+    cudaMemcpyAsync(host_out + i0 * img_out, d_out[s], static_cast<size_t>(nk * img_out) * 4,
+                    cudaMemcpyDeviceToHost, P.d2h);
+    cudaEventRecord(P.out_done[s], P.d2h);
+  }
+  // the caller's stream resumes after the last download; the call itself blocks on it
+  cudaEventRecord(P.start, P.d2h);
+  cudaStreamWaitEvent(user, P.start, 0);
+  cudaError_t e = cudaStreamSynchronize(P.d2h);
+  if (rc) return rc;  // message already set by the failing entry point
+  if (e != cudaSuccess) return im2win_set_error(2, cudaGetErrorString(e));
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return im2win_set_error(2, cudaGetErrorString(e));
+  return 0;
+}
+
+}  // extern "C"

@@ -12,6 +12,7 @@ Extra keyword `variant` (default "fp32-exact") selects the arithmetic:
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -235,3 +236,64 @@ def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, 
         conv_cl_into(win_cl, fd, out, params, variant)
         return Tensor4(out)
     return compute_from_windows_opt(im2win(i, params), f, params, plan, variant=variant)
+
+
+def _host_f32(x, ndim: int) -> torch.Tensor:
+    """A host operand as a contiguous float32 CPU tensor (no copy when it already is one)."""
+    if isinstance(x, Tensor4):
+        raise ShapeError("conv_im2win_opt_host takes host operands; use conv_im2win_opt for device tensors")
+    if hasattr(x, "data") and isinstance(getattr(x, "data"), np.ndarray):
+        x = x.data  # a reference winconv.Tensor4 (or look-alike)
+    if isinstance(x, np.ndarray):
+        x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+    if not isinstance(x, torch.Tensor):
+        raise ShapeError(f"unsupported operand type {type(x).__name__}")
+    if x.is_cuda:
+        raise ShapeError("conv_im2win_opt_host takes host operands; use conv_im2win_opt for device tensors")
+    if x.dim() != ndim:
+        raise ShapeError(f"expected a {ndim}-D array, got {x.dim()}-D")
+    if min(x.shape) < 1:
+        raise ShapeError(f"all extents must be positive, got {tuple(x.shape)}")
+    return x.to(DTYPE).contiguous()
+
+
+def conv_im2win_opt_host(inp, flt, params: ConvParams, plan: TilePlan | None = None, *,
+                         variant: str = "fp32-exact", out: torch.Tensor | None = None, chunk_images: int = 0,
+                         device=None) -> torch.Tensor:
+    """`conv_im2win_opt` for host operands, as the reference is called (optimized.py:237-241).
+
+    Host input and filter in, host output back (a CPU float32 tensor; pass a
+    page-locked `out` to reuse it).  The library cuts the batch into chunks and
+    overlaps upload, transform + conv, and download on three streams
+    (csrc/pipeline.cu); results are bit-identical to the device path.  Page-locked
+    operands let the copies overlap; pageable ones work but serialise.
+    """
+    x = _host_f32(inp, 4)
+    f = _host_f32(flt, 4)
+    n_img, c_in, h_in, w_in = (int(d) for d in x.shape)
+    if tuple(f.shape) != params.filter_dims:
+        raise ShapeError(f"filter dims {tuple(f.shape)} do not match params {params.filter_dims}")
+    if c_in != params.c_in:
+        raise ShapeError(f"input has {c_in} channels, params expect {params.c_in}")
+    h_out, w_out = output_dims(h_in, w_in, params)
+    shape = (n_img, params.c_out, h_out, w_out)
+    if out is None:
+        out = torch.empty(shape, dtype=DTYPE, pin_memory=True)
+    elif tuple(out.shape) != shape or out.dtype != DTYPE or out.is_cuda or not out.is_contiguous():
+        raise ShapeError(f"out must be a contiguous float32 host tensor of shape {shape}")
+    if not torch.cuda.is_available():
+        raise ShapeError("a CUDA device is required (this package has no CPU path)")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    code = _variant_code(variant)
+    lib = _lib.load()
+    nbytes = lib.im2win_conv_host_workspace_bytes(n_img, c_in, h_in, w_in, params.c_out, params.h_f, params.w_f,
+                                                  params.stride, code, chunk_images)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    ws = _workspace(dev, stream, nbytes)
+    cplan = to_c_plan(plan)
+    rc = lib.im2win_conv_host_f32(x.data_ptr(), f.data_ptr(), out.data_ptr(), n_img, c_in, h_in, w_in,
+                                  params.c_out, params.h_f, params.w_f, params.stride,
+                                  None if cplan is None else _byref(cplan), code, chunk_images, ws.data_ptr(),
+                                  ws.numel(), stream)
+    _lib.check(rc)
+    return out

@@ -255,3 +255,45 @@ def test_64bit_indexing_conv4_n256():
         assert bits_equal(win.data[i:i + 1].cpu().numpy(), ref_w), i
         ref = orc.conv_direct(x[i:i + 1].numpy(), flt.numpy(), cfg.stride)
         assert bits_equal(out.data[i:i + 1].cpu().numpy(), ref), i
+
+
+@pytest.mark.parametrize("name", ["conv1", "conv4", "conv9", "conv12"])
+def test_host_pipeline_matches_goldens(name, layer_goldens):
+    """conv_im2win_opt_host (numpy in -> host out, streamed chunks) gives the reference's bits."""
+    g = layer_goldens[name]
+    cfg = replace(BENCHMARKS[name], batch=g["batch"], seed=g["seed"])
+    inp, flt = make_inputs(cfg)
+    for chunk in (0, 1):
+        out = pkg.conv_im2win_opt_host(inp, flt, cfg.params, chunk_images=chunk)
+        assert not out.is_cuda
+        assert orc.checksum(out.numpy()) == g["out_sha"], (name, chunk)
+
+
+@pytest.mark.parametrize("variant", pkg.VARIANTS)
+def test_host_pipeline_equals_device_path(variant):
+    """Every chunking of the streamed host path is bit-identical to the device path (ragged last chunk)."""
+    cfg = replace(BENCHMARKS["conv10"], batch=11, seed=5)
+    inp, flt = make_inputs(cfg)
+    if variant in ("tf32", "bf16"):
+        dev = pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant, tc_path="fused").numpy()
+    else:
+        dev = pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant).numpy()
+    pinned_in = torch.from_numpy(inp).pin_memory()
+    out = torch.empty(dev.shape, dtype=torch.float32).pin_memory()
+    for chunk in (0, 1, 4, 11, 64):
+        out.fill_(float("nan"))
+        pkg.conv_im2win_opt_host(pinned_in, flt, cfg.params, variant=variant, chunk_images=chunk, out=out)
+        assert bits_equal(out.numpy(), dev), (variant, chunk)
+
+
+def test_host_pipeline_errors():
+    cfg = replace(BENCHMARKS["conv12"], batch=2, seed=1)
+    inp, flt = make_inputs(cfg)
+    with pytest.raises(pkg.ShapeError):
+        pkg.conv_im2win_opt_host(inp[:, :5], flt, cfg.params)
+    with pytest.raises(pkg.ShapeError):
+        pkg.conv_im2win_opt_host(torch.from_numpy(inp).to(DEV), flt, cfg.params)
+    with pytest.raises(pkg.GeometryError):
+        pkg.conv_im2win_opt_host(inp[:, :, :2, :2], flt, cfg.params)
+    with pytest.raises(pkg.ShapeError):
+        pkg.conv_im2win_opt_host(inp, flt, cfg.params, out=torch.empty(3))
