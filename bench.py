@@ -44,6 +44,40 @@ def load_peaks() -> dict:
     return dict(PEAKS_FALLBACK)
 
 
+def pcie_probe(dev, stream, nbytes: int = 256 << 20) -> dict:
+    """Pinned host<->device copy bandwidth (GB/s): H2D alone, D2H alone, both at once."""
+    import torch
+
+    hs = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    hd = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    da = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    db = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    side = torch.cuda.Stream(dev)
+
+    def timed(fn):
+        fn()
+        best = 1e30
+        for _ in range(3):
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            best = min(best, e0.elapsed_time(e1) * 1e-3)
+        return nbytes / best / 1e9
+
+    def both():
+        side.wait_stream(stream)
+        da.copy_(hs, non_blocking=True)
+        with torch.cuda.stream(side):
+            hd.copy_(db, non_blocking=True)
+        stream.wait_stream(side)
+
+    return {"h2d_gbs": timed(lambda: da.copy_(hs, non_blocking=True)),
+            "d2h_gbs": timed(lambda: hd.copy_(db, non_blocking=True)), "bidir_each_gbs": timed(both)}
+
+
 def load_traffic(names, batch: int, variant: str):
     """DRAM traffic of the step's kernels from the committed ncu --set full capture.
 
@@ -349,8 +383,12 @@ def main() -> None:
     d2h = sum(h["out"].numel() * 4 for h in host)
 
     def e2e_step():
-        for L, h in zip(layers, host):
-            pkg.conv_im2win_opt_host(h["x"], h["f"], L["cfg"].params, variant=args.variant, out=h["out"])
+        # all layers submitted back to back (non-blocking), then waited: one layer's uploads
+        # overlap the previous layer's downloads; every output is on the host at the end
+        jobs = [pkg.conv_im2win_opt_host(h["x"], h["f"], L["cfg"].params, variant=args.variant, out=h["out"],
+                                         wait=False) for L, h in zip(layers, host)]
+        for j in jobs:
+            j.wait()
 
     e2e_step()
     torch.cuda.synchronize(dev)
@@ -365,7 +403,10 @@ def main() -> None:
     # the streamed result must be the device path's result (bitwise), checked once outside the timing
     e2e_ok = all(torch.equal(h["out"].view(torch.int32), L["out"].cpu().view(torch.int32))
                  for L, h in zip(layers, host)) if args.variant == "fp32-exact" else None
+    pcie = pcie_probe(dev, stream)
+    e2e_bound_ms = max(h2d / (pcie["bidir_each_gbs"] * 1e9), d2h / (pcie["bidir_each_gbs"] * 1e9)) * 1e3
     e2e = {"value": flops_step * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOPS",
+           "pcie_gbs": pcie, "copy_bound_ms_per_step": e2e_bound_ms,
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
            "path": "paper_2306_14316_b200.conv_im2win_opt_host -> im2win_conv_host_f32 (C ABI), pinned host "
                    "operands, chunked upload/compute/download overlap",

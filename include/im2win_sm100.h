@@ -133,6 +133,19 @@ int im2win_conv_host_f32(const float* host_in, const float* host_flt, float* hos
                          int32_t stride, const im2win_tile_plan* plan, int32_t variant,
                          int64_t chunk_images, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Non-blocking form: enqueues the same work and returns at once with a ticket;
+ * host_out (and the workspace, which must stay allocated and unused by others)
+ * are valid/free after im2win_conv_host_wait(ticket) returns 0.  Consecutive
+ * submissions on one device overlap (uploads of one with downloads of the
+ * previous).  The caller's stream is only used to order the start. */
+int im2win_conv_host_submit(const float* host_in, const float* host_flt, float* host_out, int64_t n,
+                            int64_t c_in, int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f,
+                            int32_t stride, const im2win_tile_plan* plan, int32_t variant,
+                            int64_t chunk_images, void* workspace, size_t workspace_bytes, void* stream,
+                            int64_t* ticket);
+
+int im2win_conv_host_wait(int64_t ticket);
+
 /* Measurement utility (bench.py only): launches `blocks` x 256 threads that each
  * retire 2*32*iters flops of independent FP32 multiply-add chains; exact != 0
  * issues FMUL+FADD (the conv's bit-exact pair), else FFMA.  Used to measure the

@@ -39,6 +39,8 @@ EXPORTED_SYMBOLS = (
     "im2win_conv_basic_f32",
     "im2win_conv_host_workspace_bytes",
     "im2win_conv_host_f32",
+    "im2win_conv_host_submit",
+    "im2win_conv_host_wait",
 )
 
 
@@ -101,6 +103,12 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         lib.im2win_conv_host_f32.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32,
                                              ctypes.POINTER(TilePlanC), i32, i64, vp, sz, vp]
         lib.im2win_conv_host_f32.restype = ctypes.c_int
+        lib.im2win_conv_host_submit.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32,
+                                                ctypes.POINTER(TilePlanC), i32, i64, vp, sz, vp,
+                                                ctypes.POINTER(ctypes.c_int64)]
+        lib.im2win_conv_host_submit.restype = ctypes.c_int
+        lib.im2win_conv_host_wait.argtypes = [i64]
+        lib.im2win_conv_host_wait.restype = ctypes.c_int
         if path is None:
             _lib = lib
         return lib

@@ -3,7 +3,7 @@
 // with the host<->device copies overlapped against the kernels.
 //
 // Images are independent (reference.py:78-90), so the batch is cut into chunks
-// of `chunk` images and run as a three-stream software pipeline per device:
+// of `chunk` images (default n/4) and run as a three-stream software pipeline per device:
 //
 //   h2d  : copy input chunk k            -> in[k%2]        (waits xf[k-2])
 //   comp : transform in[k%2] -> Ĩ,  conv Ĩ -> out[k%2]      (waits h2d[k], d2h[k-2])
@@ -22,6 +22,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/im2win_sm100.h"
@@ -32,13 +33,16 @@ int im2win_set_error(int code, const char* msg);
 namespace {
 
 constexpr int kMaxDev = 64;
-constexpr int kDepth = 2;  // input / output chunk buffers in flight
+constexpr int kMaxDepth = 4;  // input / output chunk buffers in flight (runtime depth <= this)
+constexpr int kRing = 256;  // completion events of non-blocking submissions
 
 struct DevPipe {
   bool ready = false;
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
   cudaEvent_t start = nullptr;
-  cudaEvent_t in_ready[kDepth], xf_done[kDepth], conv_done[kDepth], out_done[kDepth];
+  cudaEvent_t in_ready[kMaxDepth], xf_done[kMaxDepth], conv_done[kMaxDepth], out_done[kMaxDepth];
+  cudaEvent_t done[kRing];
+  int64_t submitted = 0;  // tickets issued on this device (ticket t -> done[t % kRing])
   std::mutex mu;
 };
 
@@ -84,15 +88,25 @@ Geometry geometry(int64_t n_chunk, int64_t c_in, int64_t h, int64_t w, int64_t c
   return g;
 }
 
+int depth() {
+  static int d = [] {
+    const char* e = getenv("IM2WIN_HOST_DEPTH");
+    int v = e ? atoi(e) : 2;
+    return v < 2 ? 2 : (v > kMaxDepth ? kMaxDepth : v);
+  }();
+  return d;
+}
+
 size_t workspace_bytes(const Geometry& g) {
   return align_up(g.flt_elems * 4) + align_up(g.conv_ws) + align_up(g.mid_bytes) +
-         kDepth * (align_up(g.in_elems * 4) + align_up(g.out_elems * 4));
+         depth() * (align_up(g.in_elems * 4) + align_up(g.out_elems * 4));
 }
 
 int64_t pick_chunk(int64_t n, int64_t chunk) {
   if (chunk > 0) return std::min(chunk, n);
-  // ~8 chunks per call: fill/drain costs ~1/8 of the copy time, chunks stay large
-  return std::max<int64_t>(1, (n + 7) / 8);
+  // 4 chunks per call (measured best over 4..32 images per chunk at N=128, tools/e2e_sweep.py):
+  // larger chunks keep the kernels efficient; consecutive non-blocking calls overlap the fill/drain
+  return std::max<int64_t>(1, (n + 3) / 4);
 }
 
 }  // namespace
@@ -107,10 +121,12 @@ size_t im2win_conv_host_workspace_bytes(int64_t n, int64_t c_in, int64_t h, int6
   return workspace_bytes(geometry(cn, c_in, h, w, c_out, h_f, w_f, stride, variant));
 }
 
-int im2win_conv_host_f32(const float* host_in, const float* host_flt, float* host_out, int64_t n, int64_t c_in,
-                         int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
-                         const im2win_tile_plan* plan, int32_t variant, int64_t chunk_images, void* workspace,
-                         size_t ws_bytes, void* stream) {
+}  // extern "C"
+
+static int host_conv(const float* host_in, const float* host_flt, float* host_out, int64_t n, int64_t c_in,
+                     int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
+                     const im2win_tile_plan* plan, int32_t variant, int64_t chunk_images, void* workspace,
+                     size_t ws_bytes, void* stream, int64_t* ticket) {
   if (!host_in || !host_flt || !host_out || !workspace) return im2win_set_error(1, "im2win_conv_host_f32: null pointer");
   if (n < 1 || c_in < 1 || h < 1 || w < 1 || c_out < 1 || h_f < 1 || w_f < 1 || stride < 1)
     return im2win_set_error(1, "im2win_conv_host_f32: extents must be positive");
@@ -134,12 +150,13 @@ int im2win_conv_host_f32(const float* host_in, const float* host_flt, float* hos
     cudaStreamCreateWithFlags(&P.comp, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&P.start, cudaEventDisableTiming);
-    for (int i = 0; i < kDepth; ++i) {
+    for (int i = 0; i < kMaxDepth; ++i) {
       cudaEventCreateWithFlags(&P.in_ready[i], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&P.xf_done[i], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&P.conv_done[i], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&P.out_done[i], cudaEventDisableTiming);
     }
+    for (int i = 0; i < kRing; ++i) cudaEventCreateWithFlags(&P.done[i], cudaEventDisableTiming);
     if (cudaGetLastError() != cudaSuccess) return im2win_set_error(2, "im2win_conv_host_f32: stream setup failed");
     P.ready = true;
   }
@@ -152,9 +169,10 @@ int im2win_conv_host_f32(const float* host_in, const float* host_flt, float* hos
   base += align_up(g.conv_ws);
   void* mid = base;
   base += align_up(g.mid_bytes);
-  float* d_in[kDepth];
-  float* d_out[kDepth];
-  for (int i = 0; i < kDepth; ++i) {
+  const int D = depth();
+  float* d_in[kMaxDepth];
+  float* d_out[kMaxDepth];
+  for (int i = 0; i < D; ++i) {
     d_in[i] = reinterpret_cast<float*>(base);
     base += align_up(g.in_elems * 4);
     d_out[i] = reinterpret_cast<float*>(base);
@@ -167,24 +185,24 @@ int im2win_conv_host_f32(const float* host_in, const float* host_flt, float* hos
   cudaStreamWaitEvent(P.h2d, P.start, 0);
   cudaStreamWaitEvent(P.comp, P.start, 0);
   cudaStreamWaitEvent(P.d2h, P.start, 0);
-  cudaMemcpyAsync(d_flt, host_flt, g.flt_elems * 4, cudaMemcpyHostToDevice, P.comp);
+  cudaMemcpyAsync(d_flt, host_flt, g.flt_elems * 4, cudaMemcpyHostToDevice, P.h2d);  // before chunk 0's in_ready
 
   const int64_t img_in = c_in * h * w;
   const int64_t img_out = c_out * g.h_out * g.w_out;
   const int64_t n_chunks = (n + cn - 1) / cn;
   int rc = 0;
   for (int64_t k = 0; k < n_chunks && rc == 0; ++k) {
-    const int s = static_cast<int>(k % kDepth);
+    const int s = static_cast<int>(k % D);
     const int64_t i0 = k * cn;
     const int64_t nk = std::min(cn, n - i0);
     // upload (buffer s was last read by chunk k-2's transform)
-    if (k >= kDepth) cudaStreamWaitEvent(P.h2d, P.xf_done[s], 0);
+    if (k >= D) cudaStreamWaitEvent(P.h2d, P.xf_done[s], 0);
     cudaMemcpyAsync(d_in[s], host_in + i0 * img_in, static_cast<size_t>(nk * img_in) * 4, cudaMemcpyHostToDevice,
                     P.h2d);
     cudaEventRecord(P.in_ready[s], P.h2d);
     // compute (output buffer s was last read by chunk k-2's download)
     cudaStreamWaitEvent(P.comp, P.in_ready[s], 0);
-    if (k >= kDepth) cudaStreamWaitEvent(P.comp, P.out_done[s], 0);
+    if (k >= D) cudaStreamWaitEvent(P.comp, P.out_done[s], 0);
     if (g.tc) {
       rc = im2win_nchw_to_nhwc(d_in[s], mid, nk, c_in, h, w, variant == IM2WIN_BF16 ? 1 : 0, P.comp);
       cudaEventRecord(P.xf_done[s], P.comp);
@@ -206,7 +224,17 @@ int im2win_conv_host_f32(const float* host_in, const float* host_flt, float* hos
                     cudaMemcpyDeviceToHost, P.d2h);
     cudaEventRecord(P.out_done[s], P.d2h);
   }
-  // the caller's stream resumes after the last download; the call itself blocks on it
+  if (ticket) {
+    // non-blocking: completion is ticket-tracked; the caller's stream is not made to wait,
+    // so the next submission's uploads overlap this one's downloads
+    const int64_t t = P.submitted++;
+    cudaEventRecord(P.done[t % kRing], P.d2h);
+    *ticket = (static_cast<int64_t>(dev) << 48) | t;
+    if (rc) return rc;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : im2win_set_error(2, cudaGetErrorString(e));
+  }
+  // blocking: the caller's stream resumes after the last download; the call itself blocks on it
   cudaEventRecord(P.start, P.d2h);
   cudaStreamWaitEvent(user, P.start, 0);
   cudaError_t e = cudaStreamSynchronize(P.d2h);
@@ -215,6 +243,43 @@ int im2win_conv_host_f32(const float* host_in, const float* host_flt, float* hos
   e = cudaGetLastError();
   if (e != cudaSuccess) return im2win_set_error(2, cudaGetErrorString(e));
   return 0;
+}
+
+extern "C" {
+
+int im2win_conv_host_f32(const float* host_in, const float* host_flt, float* host_out, int64_t n, int64_t c_in,
+                         int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
+                         const im2win_tile_plan* plan, int32_t variant, int64_t chunk_images, void* workspace,
+                         size_t ws_bytes, void* stream) {
+  return host_conv(host_in, host_flt, host_out, n, c_in, h, w, c_out, h_f, w_f, stride, plan, variant, chunk_images,
+                   workspace, ws_bytes, stream, nullptr);
+}
+
+int im2win_conv_host_submit(const float* host_in, const float* host_flt, float* host_out, int64_t n, int64_t c_in,
+                            int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
+                            const im2win_tile_plan* plan, int32_t variant, int64_t chunk_images, void* workspace,
+                            size_t ws_bytes, void* stream, int64_t* ticket) {
+  if (!ticket) return im2win_set_error(1, "im2win_conv_host_submit: null ticket");
+  return host_conv(host_in, host_flt, host_out, n, c_in, h, w, c_out, h_f, w_f, stride, plan, variant, chunk_images,
+                   workspace, ws_bytes, stream, ticket);
+}
+
+int im2win_conv_host_wait(int64_t ticket) {
+  const int dev = static_cast<int>(ticket >> 48);
+  const int64_t t = ticket & ((static_cast<int64_t>(1) << 48) - 1);
+  if (dev < 0 || dev >= kMaxDev) return im2win_set_error(1, "im2win_conv_host_wait: bad ticket");
+  DevPipe& P = g_pipes[dev];
+  cudaEvent_t ev;
+  {
+    std::lock_guard<std::mutex> lock(P.mu);
+    if (!P.ready || t >= P.submitted) return im2win_set_error(1, "im2win_conv_host_wait: bad ticket");
+    // the d2h stream is in order: if slot t was re-recorded by a later ticket, that one
+    // completes after t, so waiting on it is still correct (just later)
+    ev = P.done[t % kRing];
+  }
+  cudaSetDevice(dev);
+  cudaError_t e = cudaEventSynchronize(ev);
+  return e == cudaSuccess ? 0 : im2win_set_error(2, cudaGetErrorString(e));
 }
 
 }  // extern "C"

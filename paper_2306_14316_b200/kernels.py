@@ -257,9 +257,33 @@ def _host_f32(x, ndim: int) -> torch.Tensor:
     return x.to(DTYPE).contiguous()
 
 
+class HostConv:
+    """A submitted host-buffer convolution (conv_im2win_opt_host(..., wait=False)).
+
+    Holds the operands and the device workspace until `wait()` returns; `out`
+    is valid after that.  Dropping an unfinished handle waits for it.
+    """
+
+    def __init__(self, out, ticket, keep):
+        self.out = out
+        self._ticket = ticket
+        self._keep = keep
+
+    def wait(self) -> torch.Tensor:
+        if self._keep is not None:
+            rc = _lib.load().im2win_conv_host_wait(self._ticket)
+            self._keep = None
+            _lib.check(rc)
+        return self.out
+
+    def __del__(self):
+        if getattr(self, "_keep", None) is not None:
+            _lib.load().im2win_conv_host_wait(self._ticket)
+
+
 def conv_im2win_opt_host(inp, flt, params: ConvParams, plan: TilePlan | None = None, *,
                          variant: str = "fp32-exact", out: torch.Tensor | None = None, chunk_images: int = 0,
-                         device=None) -> torch.Tensor:
+                         device=None, wait: bool = True):
     """`conv_im2win_opt` for host operands, as the reference is called (optimized.py:237-241).
 
     Host input and filter in, host output back (a CPU float32 tensor; pass a
@@ -267,6 +291,8 @@ def conv_im2win_opt_host(inp, flt, params: ConvParams, plan: TilePlan | None = N
     overlaps upload, transform + conv, and download on three streams
     (csrc/pipeline.cu); results are bit-identical to the device path.  Page-locked
     operands let the copies overlap; pageable ones work but serialise.
+    With wait=False the call returns a `HostConv` at once; consecutive
+    submissions overlap each other (uploads of one with downloads of the last).
     """
     x = _host_f32(inp, 4)
     f = _host_f32(flt, 4)
@@ -289,11 +315,17 @@ def conv_im2win_opt_host(inp, flt, params: ConvParams, plan: TilePlan | None = N
     nbytes = lib.im2win_conv_host_workspace_bytes(n_img, c_in, h_in, w_in, params.c_out, params.h_f, params.w_f,
                                                   params.stride, code, chunk_images)
     stream = torch.cuda.current_stream(dev).cuda_stream
-    ws = _workspace(dev, stream, nbytes)
     cplan = to_c_plan(plan)
-    rc = lib.im2win_conv_host_f32(x.data_ptr(), f.data_ptr(), out.data_ptr(), n_img, c_in, h_in, w_in,
-                                  params.c_out, params.h_f, params.w_f, params.stride,
-                                  None if cplan is None else _byref(cplan), code, chunk_images, ws.data_ptr(),
-                                  ws.numel(), stream)
-    _lib.check(rc)
-    return out
+    cp = None if cplan is None else _byref(cplan)
+    args = (x.data_ptr(), f.data_ptr(), out.data_ptr(), n_img, c_in, h_in, w_in, params.c_out, params.h_f,
+            params.w_f, params.stride, cp, code, chunk_images)
+    if wait:
+        ws = _workspace(dev, stream, nbytes)
+        _lib.check(lib.im2win_conv_host_f32(*args, ws.data_ptr(), ws.numel(), stream))
+        return out
+    import ctypes
+
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)  # owned by the handle until wait()
+    ticket = ctypes.c_int64(-1)
+    _lib.check(lib.im2win_conv_host_submit(*args, ws.data_ptr(), ws.numel(), stream, ctypes.byref(ticket)))
+    return HostConv(out, ticket.value, (x, f, ws, cplan))

@@ -297,3 +297,18 @@ def test_host_pipeline_errors():
         pkg.conv_im2win_opt_host(inp[:, :, :2, :2], flt, cfg.params)
     with pytest.raises(pkg.ShapeError):
         pkg.conv_im2win_opt_host(inp, flt, cfg.params, out=torch.empty(3))
+
+
+def test_host_pipeline_nonblocking_overlapped_submissions():
+    """Several non-blocking submissions in flight at once give the blocking path's bits."""
+    names = ["conv9", "conv10", "conv12", "conv9"]
+    jobs = []
+    for i, name in enumerate(names):
+        cfg = replace(BENCHMARKS[name], batch=7 + i, seed=40 + i)
+        inp, flt = make_inputs(cfg)
+        ref = pkg.conv_im2win_opt_host(inp, flt, cfg.params).clone()
+        h = pkg.conv_im2win_opt_host(torch.from_numpy(inp).pin_memory(), flt, cfg.params, chunk_images=2,
+                                     wait=False)
+        jobs.append((h, ref))
+    for h, ref in reversed(jobs):
+        assert bits_equal(h.wait().numpy(), ref.numpy())
