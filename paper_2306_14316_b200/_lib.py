@@ -8,6 +8,7 @@ cross the boundary.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -63,7 +64,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path is not None else LIB_PATH
+        # IM2WIN_LIB: an alternate build of the same library (exploration builds, tools/build_variant.sh)
+        p = Path(path) if path is not None else Path(os.environ.get("IM2WIN_LIB", LIB_PATH))
         if not p.exists():
             raise ImportError(
                 f"{p} is missing: build it with `python -m paper_2306_14316_b200.build` "

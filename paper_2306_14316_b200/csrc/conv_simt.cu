@@ -25,6 +25,13 @@
 //     quadrants so fragments are 128-bit shared loads ("vectorized load").
 #include "common.cuh"
 
+#ifndef IM2WIN_SIMT_INTERLEAVE
+#define IM2WIN_SIMT_INTERLEAVE 1
+#endif
+#ifndef IM2WIN_SIMT_SDELTA
+#define IM2WIN_SIMT_SDELTA 1
+#endif
+
 namespace im2win {
 
 struct ConvArgs {
@@ -37,6 +44,7 @@ struct ConvArgs {
   uint32_t c_in, h_out, w_out, row_len, s_hf, hw;
   FastDiv fd_hw, fd_wo;
   uint32_t m_tiles;
+  uint32_t vec_out;                 // Ho*Wo % 4 == 0: 16-byte output stores
 };
 
 // ---------------------------------------------------------------------------
@@ -73,22 +81,39 @@ IM2WIN_DEVICE float mac(float acc, float a, float b) {
   }
 }
 
-template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC, bool MB = false>
-__global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
+// MT: register micro-tile MT x MT per thread (8: two 4x4 quadrants, the paper's
+// 8x8; 4: one 4x4 quadrant, for layers too small to fill 148 SMs with 8x8 threads).
+// SD: the per-k offset table delta[] is staged in shared memory once per CTA
+// (its global-load latency otherwise sits on the gather's critical path).
+// The gather of slab kt+STAGES-1 is issued in BK/4 parts interleaved with the
+// compute of slab kt, so the 4-byte async copies do not arrive as one burst.
+template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC, int MT, bool SD>
+__global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? 2 : ((BM / MT) * (BN / MT) >= 512 ? 1 : 3))
     conv_simt_kernel(const ConvArgs a) {
-  constexpr int NT = (BM / 8) * (BN / 8);
-  constexpr int TXN = BN / 8;                 // threads along n
+  constexpr int NT = (BM / MT) * (BN / MT);
+  constexpr int TXN = BN / MT;                // threads along n
   constexpr int CPT = (BN + NT - 1) / NT;     // gather columns per thread
+  constexpr int HALVES = MT / 4;              // 4-wide quadrants per axis
+  constexpr int PARTS = BK / 4;               // gather parts per slab
   static_assert(BK % 4 == 0, "BK must be a multiple of 4 (int4 delta loads)");
+  static_assert(MT == 4 || MT == 8, "micro-tile is 4x4 or 8x8");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* As = reinterpret_cast<float*>(smem_raw);  // [STAGES][BK][BM]
   float* Bs = As + STAGES * BK * BM;               // [STAGES][BK][BN]
+  int* sdelta = reinterpret_cast<int*>(Bs + STAGES * BK * BN);  // [Kp] when SD
 
   const int tid = threadIdx.x;
   const uint32_t m_tile = blockIdx.x % a.m_tiles;
   const uint32_t n_tile = blockIdx.x / a.m_tiles;
   const int m0 = m_tile * BM;
   const uint32_t n0 = n_tile * BN;
+
+  if constexpr (SD) {
+    for (int q = tid; q < a.Kp / 4; q += NT)
+      reinterpret_cast<int4*>(sdelta)[q] = __ldg(reinterpret_cast<const int4*>(a.delta) + q);
+    __syncthreads();
+  }
+  const int* dtab = SD ? sdelta : a.delta;
 
   // Per-thread gather columns: the window-matrix column n starts at
   // src_off(n) = ((img*C*Ho + oh)*RL + ow*s*Hf) (optimized.py:101-102);
@@ -113,8 +138,8 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
   const int k_tiles = a.Kp / BK;
   const int k_full = a.K / BK;  // slabs with no padded k
 
-  auto load_stage = [&](int kt, int slot) {
-    // filter slab: BK rows of BM floats, 16-byte copies
+  // filter slab: BK rows of BM floats, 16-byte copies
+  auto load_filter = [&](int kt, int slot) {
     const float* fsrc = a.fltT + static_cast<int64_t>(kt) * BK * a.Mp + m0;
     float* adst = As + slot * BK * BM;
 #pragma unroll
@@ -122,14 +147,13 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
       int r = q / (BM / 4), c4 = q % (BM / 4);
       cp_async_16(smem_u32(adst + r * BM + c4 * 4), fsrc + static_cast<int64_t>(r) * a.Mp + c4 * 4, 16);
     }
-    // window slab: each gathering thread owns whole columns of BK elements
-    int d[BK];
-#pragma unroll
-    for (int q = 0; q < BK / 4; ++q) {
-      int4 v = __ldg(reinterpret_cast<const int4*>(a.delta + kt * BK) + q);
-      d[4 * q] = v.x; d[4 * q + 1] = v.y; d[4 * q + 2] = v.z; d[4 * q + 3] = v.w;
-    }
-    float* bdst = Bs + slot * BK * BN;
+  };
+  // window slab rows [4*part, 4*part+4): each gathering thread owns whole columns
+  auto load_window_part = [&](int kt, int slot, int part) {
+    const int4 v = SD ? *reinterpret_cast<const int4*>(dtab + kt * BK + 4 * part)
+                      : __ldg(reinterpret_cast<const int4*>(dtab + kt * BK + 4 * part));
+    const int d[4] = {v.x, v.y, v.z, v.w};
+    float* bdst = Bs + slot * BK * BN + 4 * part * BN;
     const bool full = kt < k_full;
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
@@ -137,10 +161,10 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
       if (c < BN) {
         if (full) {
 #pragma unroll
-          for (int kk = 0; kk < BK; ++kk) cp_async_4_zfill(smem_u32(bdst + kk * BN + c), bsrc[j] + d[kk], bzero[j]);
+          for (int kk = 0; kk < 4; ++kk) cp_async_4_zfill(smem_u32(bdst + kk * BN + c), bsrc[j] + d[kk], bzero[j]);
         } else {
 #pragma unroll
-          for (int kk = 0; kk < BK; ++kk) {
+          for (int kk = 0; kk < 4; ++kk) {
             const bool ok = d[kk] >= 0;
             cp_async_4_zfill(smem_u32(bdst + kk * BN + c), ok ? bsrc[j] + d[kk] : a.win, bzero[j] || !ok);
           }
@@ -148,46 +172,53 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
       }
     }
   };
+  auto load_stage = [&](int kt, int slot) {
+    load_filter(kt, slot);
+#pragma unroll
+    for (int p = 0; p < PARTS; ++p) load_window_part(kt, slot, p);
+  };
 
-  float acc[8][8];
+  float acc[MT][MT];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+    for (int j = 0; j < MT; ++j) acc[i][j] = 0.0f;
 
   const int tx = tid % TXN;
   const int ty = tid / TXN;
 
-  auto compute_stage = [&](int slot) {
+  // compute one slab; `hook(p)` runs before k-step 4p (issues prefetch part p)
+  auto compute_stage = [&](int slot, auto&& hook) {
     const float* as = As + slot * BK * BM;
     const float* bs = Bs + slot * BK * BN;
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      float fa[8], fb[8];
+      if (kk % 4 == 0) hook(kk / 4);
+      float fa[MT], fb[MT];
       if constexpr (VEC) {
-        float4 a0 = *reinterpret_cast<const float4*>(as + kk * BM + ty * 4);
-        float4 a1 = *reinterpret_cast<const float4*>(as + kk * BM + BM / 2 + ty * 4);
-        float4 b0 = *reinterpret_cast<const float4*>(bs + kk * BN + tx * 4);
-        float4 b1 = *reinterpret_cast<const float4*>(bs + kk * BN + BN / 2 + tx * 4);
-        fa[0] = a0.x; fa[1] = a0.y; fa[2] = a0.z; fa[3] = a0.w;
-        fa[4] = a1.x; fa[5] = a1.y; fa[6] = a1.z; fa[7] = a1.w;
-        fb[0] = b0.x; fb[1] = b0.y; fb[2] = b0.z; fb[3] = b0.w;
-        fb[4] = b1.x; fb[5] = b1.y; fb[6] = b1.z; fb[7] = b1.w;
+#pragma unroll
+        for (int h = 0; h < HALVES; ++h) {
+          float4 av = *reinterpret_cast<const float4*>(as + kk * BM + h * (BM / 2) + ty * 4);
+          float4 bv = *reinterpret_cast<const float4*>(bs + kk * BN + h * (BN / 2) + tx * 4);
+          fa[4 * h] = av.x; fa[4 * h + 1] = av.y; fa[4 * h + 2] = av.z; fa[4 * h + 3] = av.w;
+          fb[4 * h] = bv.x; fb[4 * h + 1] = bv.y; fb[4 * h + 2] = bv.z; fb[4 * h + 3] = bv.w;
+        }
       } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          fa[i] = as[kk * BM + ty * 4 + i];
-          fa[4 + i] = as[kk * BM + BM / 2 + ty * 4 + i];
-          fb[i] = bs[kk * BN + tx * 4 + i];
-          fb[4 + i] = bs[kk * BN + BN / 2 + tx * 4 + i];
-        }
+        for (int h = 0; h < HALVES; ++h)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            fa[4 * h + i] = as[kk * BM + h * (BM / 2) + ty * 4 + i];
+            fb[4 * h + i] = bs[kk * BN + h * (BN / 2) + tx * 4 + i];
+          }
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = mac<EXACT>(acc[i][j], fa[i], fb[j]);
+        for (int j = 0; j < MT; ++j) acc[i][j] = mac<EXACT>(acc[i][j], fa[i], fb[j]);
     }
   };
+  auto no_hook = [](int) {};
 
   if constexpr (STAGES == 1) {
     for (int kt = 0; kt < k_tiles; ++kt) {
@@ -195,46 +226,8 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
       cp_async_commit();
       cp_async_wait<0>();
       __syncthreads();
-      compute_stage(0);
+      compute_stage(0, no_hook);
       __syncthreads();
-    }
-  } else if constexpr (MB) {
-    // mbarrier ring: full[s] completes when every thread's copies for the slab in
-    // slot s have landed (cp.async.mbarrier.arrive.noinc); empty[s] when every warp
-    // has consumed it.  No CTA-wide barrier in the K loop: warps may drift up to
-    // STAGES-PD-1 slabs apart.  PD+1 slabs are in flight ahead of the consumer.
-    constexpr int PD = STAGES - 3;
-    __shared__ __align__(8) uint64_t full_bar[STAGES];
-    __shared__ __align__(8) uint64_t empty_bar[STAGES];
-    if (tid == 0) {
-#pragma unroll
-      for (int s = 0; s < STAGES; ++s) {
-        mbarrier_init(&full_bar[s], NT);
-        mbarrier_init(&empty_bar[s], NT / 32);
-      }
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s <= PD; ++s) {
-      if (s < k_tiles) {
-        load_stage(s, s);
-        cp_async_arrive_noinc(&full_bar[s]);
-      }
-    }
-    for (int kt = 0; kt < k_tiles; ++kt) {
-      const int pf = kt + PD + 1;
-      if (pf < k_tiles) {
-        const int ps = pf % STAGES;
-        if (pf >= STAGES) mbarrier_wait_parity(&empty_bar[ps], ((pf - STAGES) / STAGES) & 1);
-        load_stage(pf, ps);
-        cp_async_arrive_noinc(&full_bar[ps]);
-      }
-      const int slot = kt % STAGES;
-      mbarrier_wait_parity(&full_bar[slot], (kt / STAGES) & 1);
-      compute_stage(slot);
-      __syncwarp();
-      if ((tid & 31) == 0) mbarrier_arrive(&empty_bar[slot]);
     }
   } else {
 #pragma unroll
@@ -242,37 +235,58 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 2)
       if (s < k_tiles) load_stage(s, s);
       cp_async_commit();
     }
+    int slot = 0, pslot = STAGES - 1;
     for (int kt = 0; kt < k_tiles; ++kt) {
       cp_async_wait<STAGES - 2>();
       __syncthreads();
-      int pf = kt + STAGES - 1;
-      if (pf < k_tiles) load_stage(pf, pf % STAGES);
+      const int pf = kt + STAGES - 1;
+      const bool do_pf = pf < k_tiles;
+      // one copy of the unrolled compute body (a second, hook-less copy overflows the
+      // instruction cache: measured as no_instructions stalls)
+      if (do_pf) {
+        if (IM2WIN_SIMT_INTERLEAVE) load_filter(pf, pslot);
+        else load_stage(pf, pslot);
+      }
+      compute_stage(slot, [&](int p) {
+        if (IM2WIN_SIMT_INTERLEAVE && do_pf) load_window_part(pf, pslot, p);
+      });
       cp_async_commit();
-      compute_stage(kt % STAGES);
+      slot = slot + 1 == STAGES ? 0 : slot + 1;
+      pslot = pslot + 1 == STAGES ? 0 : pslot + 1;
     }
   }
 
-  // epilogue: scatter to NCHW (optimized.py:209-214)
-  int64_t dst_off[8];
+  // epilogue: scatter to NCHW (optimized.py:209-214).  With Ho*Wo % 4 == 0 every
+  // aligned group of 4 columns lies in one image and is 16-byte aligned: one
+  // streaming 16-byte store per (row, quadrant).
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    uint32_t n = n0 + (j < 4 ? tx * 4 + j : BN / 2 + tx * 4 + (j - 4));
-    int64_t off = -1;
-    if (n < a.n_gemm) {
+  for (int hj = 0; hj < HALVES; ++hj) {
+    const uint32_t nq = n0 + hj * (BN / 2) + tx * 4;  // first column of this quadrant
+    if (a.vec_out && nq + 3 < a.n_gemm) {
       uint32_t img, rem;
-      a.fd_hw.divmod(n, img, rem);
-      off = static_cast<int64_t>(img) * a.M * a.hw + rem;
-    }
-    dst_off[j] = off;
-  }
+      a.fd_hw.divmod(nq, img, rem);
+      float* base = a.out + static_cast<int64_t>(img) * a.M * a.hw + rem;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    int m = m0 + (i < 4 ? ty * 4 + i : BM / 2 + ty * 4 + (i - 4));
-    if (m < a.M) {
-      int64_t mo = static_cast<int64_t>(m) * a.hw;
+      for (int i = 0; i < MT; ++i) {
+        const int m = m0 + (i / 4) * (BM / 2) + ty * 4 + (i % 4);
+        if (m < a.M)
+          __stcs(reinterpret_cast<float4*>(base + static_cast<int64_t>(m) * a.hw),
+                 make_float4(acc[i][4 * hj], acc[i][4 * hj + 1], acc[i][4 * hj + 2], acc[i][4 * hj + 3]));
+      }
+    } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (dst_off[j] >= 0) a.out[dst_off[j] + mo] = acc[i][j];
+      for (int jj = 0; jj < 4; ++jj) {
+        const uint32_t n = nq + jj;
+        if (n >= a.n_gemm) continue;
+        uint32_t img, rem;
+        a.fd_hw.divmod(n, img, rem);
+        float* base = a.out + static_cast<int64_t>(img) * a.M * a.hw + rem;
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int m = m0 + (i / 4) * (BM / 2) + ty * 4 + (i % 4);
+          if (m < a.M) base[static_cast<int64_t>(m) * a.hw] = acc[i][4 * hj + jj];
+        }
+      }
     }
   }
 }
@@ -284,19 +298,23 @@ struct SimtConfig {
   int bm, bn, bk, stages;
 };
 
-template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC, bool MB = false>
+constexpr int kDeltaSmemMax = IM2WIN_SIMT_SDELTA ? 48 * 1024 : 0;  // bytes of delta[] staged in smem
+
+template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC, int MT>
 static cudaError_t launch_cfg(const ConvArgs& a0, cudaStream_t stream) {
   ConvArgs a = a0;
   a.m_tiles = (a.M + BM - 1) / BM;
   uint64_t n_tiles = (static_cast<uint64_t>(a.n_gemm) + BN - 1) / BN;
   uint64_t grid = n_tiles * a.m_tiles;
-  size_t smem = static_cast<size_t>(STAGES) * BK * (BM + BN) * 4;
-  auto kern = conv_simt_kernel<BM, BN, BK, STAGES, EXACT, VEC, MB>;
-  if (smem + 1024 > 48 * 1024) {  // + static smem (mbarriers)
+  const bool sd = static_cast<size_t>(a.Kp) * 4 <= kDeltaSmemMax;
+  size_t smem = static_cast<size_t>(STAGES) * BK * (BM + BN) * 4 + (sd ? static_cast<size_t>(a.Kp) * 4 : 0);
+  auto kern = sd ? conv_simt_kernel<BM, BN, BK, STAGES, EXACT, VEC, MT, true>
+                 : conv_simt_kernel<BM, BN, BK, STAGES, EXACT, VEC, MT, false>;
+  if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  kern<<<static_cast<unsigned>(grid), (BM / 8) * (BN / 8), smem, stream>>>(a);
+  kern<<<static_cast<unsigned>(grid), (BM / MT) * (BN / MT), smem, stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -307,17 +325,22 @@ using im2win::ConvArgs;
 // Returns the configuration index chosen for (M, n_gemm); exposed for tests/bench.
 extern "C" int im2win_simt_pick(int M, long long n_gemm, int K) {
   (void)K;
-  if (M <= 64) return 1;    // 64 x 256
-  if (M <= 96) return 2;    // 96 x 128
-  if (n_gemm < 148LL * 128 * 2) return 3;  // 128 x 64 for small-N layers (wave fill)
-  return 0;                 // 128 x 128
+  // Measured (tools/tile_sweep.py, N=128): the 64x256 8x8 tile is the fastest wherever its
+  // grid fills the GPU; 96-channel layers use 96x128.  When the last wave of 2 CTAs/SM x 148
+  // SMs would leave the GPU under 75% busy, 4x4 micro-tiles (4x the threads) win.
+  const long long slots = 148LL * 2;
+  const bool m96 = M % 64 != 0 && M % 96 == 0;
+  const long long ctas = m96 ? (M / 96) * ((n_gemm + 127) / 128) : ((M + 63) / 64) * ((n_gemm + 255) / 256);
+  const long long waves = (ctas + slots - 1) / slots;
+  if (static_cast<double>(ctas) / static_cast<double>(waves * slots) < 0.75) return m96 ? 6 : 4;
+  return m96 ? 2 : 1;
 }
 
-// Compiled CTA tiles (index = im2win_tile_plan.block_cfg).  0-3 are the
-// production tiles (all toggles compiled); 4+ are exploration tiles.
+// Compiled CTA tiles (index = im2win_tile_plan.block_cfg).  0-3: 8x8 micro-tiles
+// (all toggles compiled); 4-6: 4x4 micro-tiles (production toggles only).
 static const int kNumCfg = 7;
-static const int kBM[kNumCfg] = {128, 64, 96, 128, 64, 128, 64};
-static const int kBN[kNumCfg] = {128, 256, 128, 64, 256, 128, 256};
+static const int kBM[kNumCfg] = {128, 64, 96, 128, 64, 128, 32};
+static const int kBN[kNumCfg] = {128, 256, 128, 64, 64, 32, 128};
 static const int kBKc[kNumCfg] = {16, 16, 16, 16, 16, 16, 16};
 static const int kMaxBK = 32;
 
@@ -338,7 +361,7 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
     *err = "im2win_conv_f32: unknown tile configuration";
     return 1;
   }
-  if (cfg >= 4 && !(exact && vec && stages > 1)) cfg = im2win_simt_pick(static_cast<int>(c_out), n_gemm, static_cast<int>(K));
+  if (cfg >= 4 && !(vec && stages > 1)) cfg = static_cast<int>(c_out) <= 64 ? 1 : 0;  // ablations: 8x8 tiles
   const int BM = kBM[cfg], BK = kBKc[cfg];
   const int Mp = static_cast<int>((c_out + BM - 1) / BM * BM);
   const int Kp = static_cast<int>((K + BK - 1) / BK * BK);
@@ -365,24 +388,29 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
   a.hw = static_cast<uint32_t>(hw);
   a.fd_hw = FastDiv(static_cast<uint32_t>(hw));
   a.fd_wo = FastDiv(static_cast<uint32_t>(w_out));
+  a.vec_out = (hw % 4 == 0) ? 1u : 0u;
 
   cudaError_t e = cudaSuccess;
 #define IM2WIN_DISPATCH(BM_, BN_, BK_)                                                              \
-  if (exact && vec && stages == 3) e = launch_cfg<BM_, BN_, BK_, 3, true, true>(a, stream);          \
-  else if (exact && vec && stages == 1) e = launch_cfg<BM_, BN_, BK_, 1, true, true>(a, stream);     \
-  else if (exact && !vec) e = launch_cfg<BM_, BN_, BK_, 3, true, false>(a, stream);                  \
-  else if (!exact && vec) e = launch_cfg<BM_, BN_, BK_, 3, false, true>(a, stream);               \
-  else e = launch_cfg<BM_, BN_, BK_, 3, false, false>(a, stream);
+  if (exact && vec && stages == 3) e = launch_cfg<BM_, BN_, BK_, 3, true, true, 8>(a, stream);       \
+  else if (exact && vec && stages == 1) e = launch_cfg<BM_, BN_, BK_, 1, true, true, 8>(a, stream);  \
+  else if (exact && !vec) e = launch_cfg<BM_, BN_, BK_, 3, true, false, 8>(a, stream);               \
+  else if (!exact && vec) e = launch_cfg<BM_, BN_, BK_, 3, false, true, 8>(a, stream);               \
+  else e = launch_cfg<BM_, BN_, BK_, 3, false, false, 8>(a, stream);
+#define IM2WIN_DISPATCH4(BM_, BN_, BK_)                                                             \
+  if (exact) e = launch_cfg<BM_, BN_, BK_, 3, true, true, 4>(a, stream);                            \
+  else e = launch_cfg<BM_, BN_, BK_, 3, false, true, 4>(a, stream);
   switch (cfg) {
     case 0: { IM2WIN_DISPATCH(128, 128, 16) break; }
     case 1: { IM2WIN_DISPATCH(64, 256, 16) break; }
     case 2: { IM2WIN_DISPATCH(96, 128, 16) break; }
     case 3: { IM2WIN_DISPATCH(128, 64, 16) break; }
-    case 4: e = launch_cfg<64, 256, 16, 4, true, true, true>(a, stream); break;   // mbarrier ring (explored)
-    case 5: e = launch_cfg<128, 128, 16, 4, true, true, true>(a, stream); break;  // mbarrier ring (explored)
-    case 6: e = launch_cfg<64, 256, 16, 5, true, true, true>(a, stream); break;  // deeper mbarrier ring
+    case 4: { IM2WIN_DISPATCH4(64, 64, 16) break; }
+    case 5: { IM2WIN_DISPATCH4(128, 32, 16) break; }
+    case 6: { IM2WIN_DISPATCH4(32, 128, 16) break; }
     default: *err = "im2win_conv_f32: unknown tile configuration"; return 1;
   }
+#undef IM2WIN_DISPATCH4
 #undef IM2WIN_DISPATCH
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);

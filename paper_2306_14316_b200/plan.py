@@ -112,25 +112,32 @@ def default_plan(dims: GemmDims) -> TilePlan:
 
 
 # CTA tiles compiled into the FP32 CUDA-core kernel (csrc/conv_simt.cu), index = block_cfg.
+# SIMT_TILES use 8x8 register micro-tiles (every TilePlan toggle compiled); SIMT_TILES_MT4
+# (block_cfg 4..6) use 4x4 micro-tiles for layers too small to fill the GPU with 8x8 threads.
 SIMT_TILES = ((128, 128), (64, 256), (96, 128), (128, 64))
-SIMT_K_SLAB = 8
+SIMT_TILES_MT4 = ((64, 64), (128, 32), (32, 128))
+SIMT_K_SLAB = 16
 SIMT_MICRO_TILE = (8, 8)
 
 
 def simt_tile_for(dims: GemmDims) -> int:
     """Library's shape-based tile choice (mirrors im2win_simt_pick in csrc/conv_simt.cu)."""
-    if dims.m <= 64:
-        return 1
-    if dims.m <= 96:
-        return 2
-    if dims.n < 148 * 128 * 2:
-        return 3
-    return 0
+    slots = 148 * 2
+    m96 = dims.m % 64 != 0 and dims.m % 96 == 0
+    ctas = (dims.m // 96) * -(-dims.n // 128) if m96 else -(-dims.m // 64) * -(-dims.n // 256)
+    waves = -(-ctas // slots)
+    if ctas / (waves * slots) < 0.75:
+        return 6 if m96 else 4
+    return 2 if m96 else 1
 
 
 def gpu_plan(dims: GemmDims) -> TilePlan:
     """The TilePlan the GPU library runs for `dims` when no plan is given."""
-    bm, bn = SIMT_TILES[simt_tile_for(dims)]
+    cfg = simt_tile_for(dims)
+    if cfg >= len(SIMT_TILES):
+        bm, bn = SIMT_TILES_MT4[cfg - len(SIMT_TILES)]
+        return TilePlan(m_b=bm, n_b=bn, k_b=SIMT_K_SLAB, m_t=4, n_t=4)
+    bm, bn = SIMT_TILES[cfg]
     return TilePlan(m_b=bm, n_b=bn, k_b=SIMT_K_SLAB, m_t=8, n_t=8)
 
 
@@ -143,5 +150,7 @@ def to_c_plan(plan: TilePlan | None):
     cfg = -1
     if (plan.m_b, plan.n_b) in SIMT_TILES and plan.m_t == 8 and plan.n_t == 8:
         cfg = SIMT_TILES.index((plan.m_b, plan.n_b))
+    elif (plan.m_b, plan.n_b) in SIMT_TILES_MT4 and plan.m_t == 4 and plan.n_t == 4:
+        cfg = len(SIMT_TILES) + SIMT_TILES_MT4.index((plan.m_b, plan.n_b))
     return TilePlanC(cfg, int(plan.micro_kernel), int(plan.vectorized_load),
                      int(plan.prefetch_double_buffer))

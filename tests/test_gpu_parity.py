@@ -68,6 +68,10 @@ def test_all_tiles_and_toggles_bitwise(small_cases):
                                             prefetch_double_buffer=pf)
                         out = pkg.compute_from_windows_opt(w, flt, _params(c), plan)
                         assert bits_equal_nan_as_class(out.numpy(), c["out"]), (name, plan)
+        for (bm, bn) in pkg.plan.SIMT_TILES_MT4:
+            plan = pkg.TilePlan(bm, bn, 8, 4, 4)
+            out = pkg.compute_from_windows_opt(w, flt, _params(c), plan)
+            assert bits_equal_nan_as_class(out.numpy(), c["out"]), (name, plan)
 
 
 @pytest.mark.parametrize("name", list(BENCHMARKS))
@@ -84,6 +88,10 @@ def test_layer_checksums_bitwise(name, layer_goldens):
         o2 = pkg.compute_from_windows_opt(w, torch.from_numpy(flt).to(DEV), cfg.params,
                                           pkg.TilePlan(bm, bn, 8, 8, 8))
         assert o2 == out, (name, bm, bn)
+    for (bm, bn) in pkg.plan.SIMT_TILES_MT4:
+        o2 = pkg.compute_from_windows_opt(w, torch.from_numpy(flt).to(DEV), cfg.params,
+                                          pkg.TilePlan(bm, bn, 8, 4, 4))
+        assert o2 == out, (name, bm, bn, "mt4")
 
 
 def test_config1_checksum(layer_goldens):

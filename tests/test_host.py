@@ -122,3 +122,22 @@ def test_c_abi_library_exports_every_header_symbol():
 def test_no_cpu_fallback():
     with pytest.raises(pkg.ShapeError, match="CUDA"):
         pkg.Tensor4(np.zeros((1, 1, 4, 4), np.float32))
+
+
+def test_tile_pick_mirrors_library():
+    """plan.simt_tile_for restates im2win_simt_pick (csrc/conv_simt.cu); no GPU call involved."""
+    import ctypes
+
+    from paper_2306_14316_b200 import _lib
+
+    lib = _lib.load()
+    lib.im2win_simt_pick.argtypes = [ctypes.c_int, ctypes.c_longlong, ctypes.c_int]
+    lib.im2win_simt_pick.restype = ctypes.c_int
+    for batch in (1, 2, 8, 32, 128, 256):
+        for name, cfg in pkg.BENCHMARKS.items():
+            d = cfg.gemm_dims()
+            d = pkg.GemmDims(d.m, d.n // cfg.batch * batch, d.k)
+            assert simt_tile_for(d) == lib.im2win_simt_pick(d.m, d.n, d.k), (name, batch)
+    for m in (1, 32, 64, 96, 100, 192, 512):
+        for n in (1, 1000, 10 ** 5, 3 * 10 ** 6):
+            assert simt_tile_for(pkg.GemmDims(m, n, 9)) == lib.im2win_simt_pick(m, n, 9), (m, n)

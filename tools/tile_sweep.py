@@ -13,7 +13,8 @@ from paper_2306_14316_b200.workloads import BENCHMARKS  # noqa: E402
 
 layers = sys.argv[1].split(",") if len(sys.argv) > 1 else ["conv4", "conv8", "conv9", "conv5", "conv6", "conv12", "conv1", "conv7"]
 cfgs = range(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
-lib = _lib.load()
+import os  # noqa: E402
+lib = _lib.load(os.environ.get("IM2WIN_LIB")) if os.environ.get("IM2WIN_LIB") else _lib.load()
 dev = torch.device("cuda:0")
 stream = torch.cuda.current_stream().cuda_stream
 for name in layers:
@@ -47,10 +48,11 @@ for name in layers:
         best = 1e9
         for _ in range(3):
             e0.record()
-            run()
+            for _ in range(5):
+                run()
             e1.record()
             torch.cuda.synchronize()
-            best = min(best, e0.elapsed_time(e1))
+            best = min(best, e0.elapsed_time(e1) / 5)
         if ref is None:
             ref = out.clone()
         same = torch.equal(out.view(torch.int32), ref.view(torch.int32))
