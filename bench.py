@@ -44,6 +44,23 @@ def load_peaks() -> dict:
     return dict(PEAKS_FALLBACK)
 
 
+def set_fp32_precision(mode: str) -> None:
+    """Float32 conv/matmul precision of the PyTorch baselines: "ieee" (true FP32) or "tf32".
+
+    torch 2.11 defaults cuDNN convolutions to TF32 (torch.backends.cudnn.conv.fp32_precision
+    == "tf32"); allow_tf32 = False alone leaves that default in place.
+    """
+    import torch
+
+    conv = getattr(torch.backends.cudnn, "conv", None)
+    if conv is not None and hasattr(conv, "fp32_precision"):
+        conv.fp32_precision = mode
+        torch.backends.cuda.matmul.fp32_precision = mode
+    else:
+        torch.backends.cudnn.allow_tf32 = mode == "tf32"
+        torch.backends.cuda.matmul.allow_tf32 = mode == "tf32"
+
+
 def pcie_probe(dev, stream, nbytes: int = 256 << 20) -> dict:
     """Pinned host<->device copy bandwidth (GB/s): H2D alone, D2H alone, both at once."""
     import torch
@@ -241,8 +258,7 @@ def main() -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dev = torch.device("cuda", local_rank if world > 1 else 0)
     torch.cuda.set_device(dev)
-    torch.backends.cuda.matmul.allow_tf32 = False
-    torch.backends.cudnn.allow_tf32 = False
+    set_fp32_precision("ieee")
 
     def barrier():
         if world > 1:
@@ -451,16 +467,39 @@ def main() -> None:
                 return torch.matmul(L["f"].view(cfg.c_out, -1), cols)
 
             ours = lambda: pkg.conv_im2win_opt(L["x"], L["f"], cfg.params, variant=args.variant)  # noqa: E731
+            # true FP32 (IEEE) cuDNN and im2col+cuBLAS, then cuDNN TF32 and BF16 for the TC variants
+            set_fp32_precision("ieee")
             t_cudnn = timed(cudnn)
             t_col = timed(im2col_cublas)
+            ref = L["out"]  # this layer's fp32-exact output from the timed region (= the reference's bits)
             rec["cudnn_tflops"] = cfg.flops / (t_cudnn * 1e-3) / 1e12
+            rec["cudnn_max_rel_diff"] = pkg.max_rel_diff(cudnn(), ref)
             rec["im2col_cublas_tflops"] = cfg.flops / (t_col * 1e-3) / 1e12
+            set_fp32_precision("tf32")
+            rec["cudnn_tf32_tflops"] = cfg.flops / (timed(cudnn) * 1e-3) / 1e12
+            rec["cudnn_tf32_norm_diff"] = pkg.normalized_max_diff(cudnn(), ref)
+            set_fp32_precision("ieee")
+            xb, fb = L["x"].to(torch.bfloat16), L["f"].to(torch.bfloat16)
+            cudnn_bf16 = lambda: F.conv2d(xb, fb, stride=cfg.stride)  # noqa: E731
+            rec["cudnn_bf16_tflops"] = cfg.flops / (timed(cudnn_bf16) * 1e-3) / 1e12
+            rec["cudnn_bf16_norm_diff"] = pkg.normalized_max_diff(cudnn_bf16().float(), ref)
+            del xb, fb
             rec["peak_mem_bytes"] = {"im2win": peak_mem(ours), "cudnn": peak_mem(cudnn),
                                      "im2col_cublas_full_batch": peak_mem(im2col_cublas)}
             torch.cuda.empty_cache()
         tot = sum(L["cfg"].flops for L in layers)
-        baselines["cudnn_tflops_step"] = tot / sum(L["cfg"].flops / (r["cudnn_tflops"] * 1e12) for L, r in zip(layers, per_layer)) / 1e12
-        baselines["im2col_cublas_tflops_step"] = tot / sum(L["cfg"].flops / (r["im2col_cublas_tflops"] * 1e12) for L, r in zip(layers, per_layer)) / 1e12
+
+        def step_tf(key):
+            return tot / sum(L["cfg"].flops / (r[key] * 1e12) for L, r in zip(layers, per_layer)) / 1e12
+
+        baselines["cudnn_tflops_step"] = step_tf("cudnn_tflops")
+        baselines["im2col_cublas_tflops_step"] = step_tf("im2col_cublas_tflops")
+        baselines["cudnn_tf32_tflops_step"] = step_tf("cudnn_tf32_tflops")
+        baselines["cudnn_bf16_tflops_step"] = step_tf("cudnn_bf16_tflops")
+        baselines["note"] = ("cudnn/im2col_cublas: torch FP32 with fp32_precision='ieee' (true FP32; cuDNN picks "
+                             "its fastest algorithm, incl. Winograd/FFT, benchmark=True); cudnn_tf32: "
+                             "fp32_precision='tf32'; cudnn_bf16: bf16 operands.  *_max_rel_diff / *_norm_diff "
+                             "are against the fp32-exact output (the reference's bits)")
 
     # ---- CPU baseline: the oracle port on the host cores, bounded sample (rank 0, N=1 only) ----
     cpu_baseline = None
