@@ -399,6 +399,10 @@ int im2win_try_conv_tc_shift(const void* x_cl, const float* flt, float* out, voi
                              int64_t c_pad, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride, int bf16,
                              double fused_util, cudaStream_t stream, const char** err);
 
+int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n, int64_t c_in,
+                             int64_t c_pad, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride, int bf16,
+                             double fused_util, cudaStream_t stream, const char** err);
+
 int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n,
                                 int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride,
                                 int bf16, cudaStream_t stream, const char** err) {
@@ -432,6 +436,13 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
   a.n_tiles = (a.n_img + a.box_n - 1) / a.box_n;
   a.fh_slabs = static_cast<uint32_t>(Kfh / bk);
   a.k_slabs = a.fh_slabs * h_f;
+  {
+    // the phase kernel reuses each loaded A tile for every tap of a stride phase (any stride <= 2)
+    const double util = static_cast<double>(a.box_w) * a.box_h * a.box_n / kTileM;
+    const int rc = im2win_try_conv_tc_phase(x_cl, flt, out, workspace, n, c_in, cp, h, w, c_out, h_f, w_f, stride,
+                                            bf16, util, stream, err);
+    if (rc != 0) return rc > 0 ? 0 : -rc;
+  }
   {
     // stride-1 layers: the window-shift kernel reuses each loaded A tile for all Wf taps
     const double util = static_cast<double>(a.box_w) * a.box_h * a.box_n / kTileM;

@@ -1,0 +1,421 @@
+// Phase-shift tensor-core convolution: the im2win window reuse for any stride, two
+// pixel tiles per CTA work item.
+//
+// im2win stores each output row's windows so that consecutive windows overlap
+// (layouts.py:73-83; test_layouts.py:187-199).  With stride s, filter tap fw = s*q + r
+// (phase r < s, shift q) reads input column s*(ow + q) + r, so the A tile of tap fw is
+// the phase-r column sequence P_r[j] = X[.., s*j + r, :] shifted by q rows.  One TMA box
+// per (fh, phase, channel chunk) therefore feeds all ceil((Wf - r)/s) taps of that phase
+// through smem descriptors advanced by q rows (q * 128 B): A is fetched Wf/s times less
+// often than by the generic fused kernel (conv_tc_fused.cu), which fetches it per tap.
+// Each work item holds MT = 2 pixel tiles (two UMMA M=128 accumulators in TMEM) so every
+// staged filter tile feeds two MMAs: filter traffic from L2 halves as well.
+//
+//   A map (one per phase r): {c, j, fh % s, (oh*s + fh) / s, n} over the channels-last
+//     copy Xcl, strides {1, s*C, W*C, s*W*C, H*W*C} elements, base Xcl + r*C;
+//     box {BK, pitch, 1, rows, box_n}, pitch = box_w + qmax, qmax = (Wf - 1) / s.
+//   B: the packed filter B[m][(fh*Wf + fw)*Kc + c] (pack_filter_shift_kernel).
+//   K loop: fh, phase r, channel chunk -> nq(r) taps x BK/UK MMAs x MT tiles.
+// D rows whose column position in the pitch is >= box_w are padding and are not stored.
+#include <stddef.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "tc_common.cuh"
+
+namespace im2win {
+namespace tc {
+
+struct PhaseArgs {
+  float* __restrict__ out;
+  uint32_t n_img, h_out, w_out, hw, co;
+  uint32_t box_w, pitch, rows, box_n;  // pixel tile: box_n images x rows output rows x box_w columns
+  uint32_t ow_tiles, oh_tiles, n_tiles, p_tiles, pairs, co_tiles;
+  uint32_t stride, w_f, c_slabs, k_iters;  // k_iters = Hf * stride * c_slabs
+};
+
+constexpr int kPhRows = 136;  // 128 MMA rows + up to 8 rows of shift
+
+template <bool BF16, int N, int STAGES, int TAPS, int MT>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    conv_tc_phase_kernel(const PhaseArgs a, const __grid_constant__ CUtensorMap tmap_a0,
+                         const __grid_constant__ CUtensorMap tmap_a1, const __grid_constant__ CUtensorMap tmap_b) {
+  constexpr uint32_t kATile = kPhRows * kRowBytes;  // 17 KB, multiple of 1024
+  constexpr uint32_t kABytes = MT * kATile;
+  constexpr uint32_t kBTap = N * kRowBytes;
+  constexpr uint32_t kStageBytes = kABytes + TAPS * kBTap;
+  constexpr int kBK = BF16 ? 64 : 32;
+  constexpr int kUK = BF16 ? 16 : 8;
+  constexpr uint32_t kTmemCols = (2 * MT * N <= 128) ? 128 : (2 * MT * N <= 256 ? 256 : 512);
+  constexpr uint32_t kIdesc = instr_desc<BF16, N>();
+  static_assert(kATile % 1024 == 0, "A tiles must keep 1024 B alignment");
+  static_assert(2 * MT * N <= 512, "TMEM holds 512 fp32 columns");
+
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t tfull_bar[2];
+  __shared__ __align__(8) uint64_t tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t loaded_rows = a.pitch * a.rows * a.box_n;
+  const uint32_t a_box_bytes = loaded_rows * kRowBytes;
+  const uint32_t s = a.stride;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], kEpiWarps);
+    }
+    fence_barrier_init();
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap_a0) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap_a1) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap_b) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  // rows past the TMA box feed only padding D rows; keep them finite
+  for (uint32_t i = threadIdx.x; i < STAGES * kStageBytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+  const uint32_t total = a.pairs * a.co_tiles;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+        const uint32_t co_blk = t % a.co_tiles;
+        const uint32_t pair = t / a.co_tiles;
+        uint32_t ow0[MT], oh0[MT], n0[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          // past the last pixel tile: coordinates past the tensor (TMA zero-fills), D not stored
+          uint32_t pt = pair * MT + mt;
+          ow0[mt] = (pt % a.ow_tiles) * a.box_w;
+          pt /= a.ow_tiles;
+          oh0[mt] = (pt % a.oh_tiles) * a.rows;
+          n0[mt] = (pt / a.oh_tiles) * a.box_n;
+        }
+        for (uint32_t ki = 0; ki < a.k_iters; ++ki) {
+          const uint32_t c0 = (ki % a.c_slabs) * kBK;
+          const uint32_t rem = ki / a.c_slabs;
+          const uint32_t r = rem % s, fh = rem / s;
+          const uint32_t nq = (a.w_f - r + s - 1) / s;
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* st = smem + stage * kStageBytes;
+          mbar_arrive_expect_tx(&full_bar[stage], MT * a_box_bytes + nq * kBTap);
+          const CUtensorMap* am = r == 0 ? &tmap_a0 : &tmap_a1;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            asm volatile(
+                "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+                "%6, %7}], [%2];\n" ::"r"(smem_u32(st + mt * kATile)),
+                "l"(am), "r"(smem_u32(&full_bar[stage])), "r"(c0), "r"(ow0[mt]), "r"(fh % s), "r"(oh0[mt] + fh / s),
+                "r"(n0[mt])
+                : "memory");
+          }
+          for (uint32_t q = 0; q < nq; ++q)
+            tma_load_2d(st + kABytes + q * kBTap, &tmap_b, &full_bar[stage],
+                        (fh * a.w_f + s * q + r) * a.c_slabs * kBK + c0, co_blk * N);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * (MT * N);
+        for (uint32_t ki = 0; ki < a.k_iters; ++ki) {
+          const uint32_t r = (ki / a.c_slabs) % s;
+          const uint32_t nq = (a.w_f - r + s - 1) / s;
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t abase = smem_u32(smem + stage * kStageBytes);
+          const uint32_t bbase = abase + kABytes;
+#pragma unroll
+          for (int q = 0; q < TAPS; ++q) {
+            if (q < static_cast<int>(nq)) {
+#pragma unroll
+              for (int kk = 0; kk < kBK / kUK; ++kk) {
+                const uint64_t bd = smem_desc_sw128(bbase + q * kBTap + kk * 32);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt)
+                  mma<BF16>(tmem_d + mt * N, smem_desc_sw128(abase + mt * kATile + q * kRowBytes + kk * 32), bd,
+                            kIdesc, (ki | q | kk) != 0);
+              }
+            }
+          }
+          mma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull_bar[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // kEpiWarps epilogue warps: warp w reads TMEM lane quarter w % 4 and column half (w - 4) / 4
+    const int quarter = warp % 4;
+    const int j_lo = ((warp - 4) / 4) * (N / 2);
+    const uint32_t rr = quarter * 32 + lane;
+    const uint32_t per_img = a.pitch * a.rows;
+    const uint32_t r_n = rr / per_img, r_rem = rr % per_img;
+    const uint32_t r_h = r_rem / a.pitch, r_w = r_rem % a.pitch;
+    uint32_t acc = 0, acc_phase = 0;
+    for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+      const uint32_t co_blk = t % a.co_tiles;
+      const uint32_t pair = t / a.co_tiles;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        uint32_t pt = pair * MT + mt;
+        const bool tile_ok = pt < a.p_tiles;
+        const uint32_t ow = (pt % a.ow_tiles) * a.box_w + r_w;
+        pt /= a.ow_tiles;
+        const uint32_t oh = (pt % a.oh_tiles) * a.rows + r_h;
+        const uint32_t img = (pt / a.oh_tiles) * a.box_n + r_n;
+        const bool valid =
+            tile_ok && rr < loaded_rows && r_w < a.box_w && ow < a.w_out && oh < a.h_out && img < a.n_img;
+        const int64_t obase =
+            valid ? static_cast<int64_t>(img) * a.co * a.hw + static_cast<int64_t>(oh) * a.w_out + ow : 0;
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * (MT * N) + mt * N;
+#pragma unroll
+        for (int jj = 0; jj < N / 2; jj += 16) {
+          const int j0 = j_lo + jj;
+          uint32_t v[16];
+          tmem_ld16(taddr + j0, v);
+          const uint32_t m0 = co_blk * N + j0;
+          if (valid) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (m0 + q < a.co) a.out[obase + static_cast<int64_t>(m0 + q) * a.hw] = __uint_as_float(v[q]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(kTmemCols));
+  }
+}
+
+// Pixel tile for the phase kernel; returns the fraction of the 128 MMA rows that are real outputs.
+inline double phase_tile(int64_t n, int64_t h_out, int64_t w_out, int64_t qmax, PhaseArgs& a) {
+  const int64_t max_w = kTileM - qmax;
+  if (w_out <= max_w) {
+    a.box_w = static_cast<uint32_t>(w_out);
+    a.pitch = static_cast<uint32_t>(w_out + qmax);
+    const int64_t rmax = std::max<int64_t>(1, kTileM / a.pitch);
+    a.rows = static_cast<uint32_t>(std::min<int64_t>(h_out, rmax));
+    a.box_n = a.rows == h_out
+                  ? static_cast<uint32_t>(std::max<int64_t>(1, std::min<int64_t>(n, kTileM / (a.pitch * h_out))))
+                  : 1u;
+  } else {
+    const int64_t parts = (w_out + max_w - 1) / max_w;
+    a.box_w = static_cast<uint32_t>((w_out + parts - 1) / parts);
+    a.pitch = static_cast<uint32_t>(a.box_w + qmax);
+    a.rows = 1;
+    a.box_n = 1;
+  }
+  return static_cast<double>(a.box_w) * a.rows * a.box_n / kTileM;
+}
+
+template <bool BF16, int N, int STAGES, int TAPS, int MT>
+static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64_t c_pad, int64_t h, int64_t w,
+                        int64_t Mp, int64_t Kp, cudaStream_t stream, const char** err) {
+  constexpr int kBK = BF16 ? 64 : 32;
+  auto enc = get_encode_fn();
+  if (!enc) {
+    *err = "conv_tc_phase: cuTensorMapEncodeTiled unavailable";
+    return 2;
+  }
+  const cuuint64_t esz = BF16 ? 2 : 4;
+  const CUtensorMapDataType dt = BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const int64_t s = a.stride;
+  CUtensorMap map_a[2], map_b;
+  for (int r = 0; r < 2; ++r) {
+    const int rr = r < s ? r : 0;  // unused second map for stride 1
+    cuuint64_t dims[5] = {static_cast<cuuint64_t>(c_pad), static_cast<cuuint64_t>((w - rr + s - 1) / s),
+                          static_cast<cuuint64_t>(s), static_cast<cuuint64_t>((h + s - 1) / s), a.n_img};
+    cuuint64_t strides[4] = {static_cast<cuuint64_t>(s * c_pad) * esz, static_cast<cuuint64_t>(w * c_pad) * esz,
+                             static_cast<cuuint64_t>(s * w * c_pad) * esz, static_cast<cuuint64_t>(h * w * c_pad) * esz};
+    cuuint32_t box[5] = {static_cast<cuuint32_t>(kBK), a.pitch, 1, a.rows, a.box_n};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    const char* base = static_cast<const char*>(x_cl) + rr * c_pad * esz;
+    CUresult res = enc(&map_a[r], dt, 5, const_cast<char*>(base), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) {
+      *err = "conv_tc_phase: input tensor map rejected (cuTensorMapEncodeTiled)";
+      return 2;
+    }
+  }
+  {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(Mp)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(Kp) * esz};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(N)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult res = enc(&map_b, dt, 2, const_cast<void*>(packed), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) {
+      *err = "conv_tc_phase: filter tensor map rejected (cuTensorMapEncodeTiled)";
+      return 2;
+    }
+  }
+  a.co_tiles = static_cast<uint32_t>(Mp / N);
+  const size_t smem = static_cast<size_t>(STAGES) * (MT * kPhRows + TAPS * N) * kRowBytes + 1024;
+  auto kern = conv_tc_phase_kernel<BF16, N, STAGES, TAPS, MT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 2;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t items = static_cast<uint64_t>(a.pairs) * a.co_tiles;
+  const uint32_t grid = items < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(items) : static_cast<uint32_t>(sms);
+  kern<<<grid, kTcThreads, smem, stream>>>(a, map_a[0], map_a[1], map_b);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 2;
+  }
+  return 0;
+}
+
+// B[m][(fh*Wf + fw)*Kc + c] = F[m][c][fh][fw] (zero for c >= C) -- same packing as the shift kernel.
+template <bool BF16>
+__global__ void pack_filter_phase_kernel(const float* __restrict__ flt, void* __restrict__ packed, int M, int C,
+                                         int h_f, int w_f, int Mp, int Kc) {
+  const int64_t Kp = static_cast<int64_t>(h_f) * w_f * Kc;
+  const int64_t total = Mp * Kp;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(i / Kp);
+    const int64_t kp = i % Kp;
+    const int tap = static_cast<int>(kp / Kc), c = static_cast<int>(kp % Kc);
+    const int fh = tap / w_f, fw = tap % w_f;
+    float v = 0.0f;
+    if (m < M && c < C) v = flt[((static_cast<int64_t>(m) * C + c) * h_f + fh) * w_f + fw];
+    if constexpr (BF16) {
+      reinterpret_cast<__nv_bfloat16*>(packed)[i] = __float2bfloat16_rn(v);
+    } else {
+      uint32_t r;
+      asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(v));
+      reinterpret_cast<uint32_t*>(packed)[i] = r;
+    }
+  }
+}
+
+}  // namespace tc
+}  // namespace im2win
+
+// Returns 1 and launches when the phase kernel applies, 0 when the caller should try the
+// next kernel, <0 on error.  Applies to stride 1-2, Wf in {3, 5, 7}, channel pitch >= 32
+// (a K-slab is one channel chunk of one tap), Co <= 128.
+int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n, int64_t c_in,
+                             int64_t c_pad, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride, int bf16,
+                             double fused_util, cudaStream_t stream, const char** err) {
+  using namespace im2win::tc;
+  const char* env = getenv("IM2WIN_PHASE");
+  const int mode = env ? atoi(env) : 1;  // 0: off, 1: auto, 2: force where legal (tests)
+  if (mode == 0) return 0;
+  // measured (tools/tc_kernels.py, N=128): stride 2 (conv4) 1.35x over the generic fused
+  // kernel; at stride 1 the single-tile shift kernel (conv_tc_shift.cu) is as fast or faster
+  if (mode == 1 && stride == 1) return 0;
+  if (stride < 1 || stride > 2 || (w_f != 3 && w_f != 5 && w_f != 7) || c_out > 128) return 0;
+  const int bk = bf16 ? 64 : 32;
+  if (c_pad < 32) return 0;
+  const int64_t h_out = (h - h_f) / stride + 1, w_out = (w - w_f) / stride + 1;
+  const int64_t qmax = (w_f - 1) / stride;
+  const int taps = (w_f + stride - 1) / stride;
+  PhaseArgs a{};
+  a.out = out;
+  a.n_img = static_cast<uint32_t>(n);
+  a.h_out = static_cast<uint32_t>(h_out);
+  a.w_out = static_cast<uint32_t>(w_out);
+  a.hw = static_cast<uint32_t>(h_out * w_out);
+  a.co = static_cast<uint32_t>(c_out);
+  const double util = phase_tile(n, h_out, w_out, qmax, a);
+  if (mode == 1 && util + 1e-9 < fused_util * 0.9) return 0;
+  const int N = c_out <= 64 ? 64 : 128;
+  if (N == 128 && taps >= 5) return 0;  // a stage would not fit twice in shared memory
+  // boxes of several output rows may overhang the last row; with h % s != 0 the phase view
+  // could then address one row past the tensor -- keep to whole-row tiles there
+  if (h % stride != 0 && a.rows > 1 && h_out % a.rows != 0) return 0;
+  const int64_t c_slabs = (c_pad + bk - 1) / bk;
+  const int64_t Kc = c_slabs * bk;
+  const int64_t Kp = static_cast<int64_t>(h_f) * w_f * Kc;
+  const int64_t Mp = (c_out + N - 1) / N * N;
+  a.ow_tiles = (a.w_out + a.box_w - 1) / a.box_w;
+  a.oh_tiles = (a.h_out + a.rows - 1) / a.rows;
+  a.n_tiles = (a.n_img + a.box_n - 1) / a.box_n;
+  a.p_tiles = a.ow_tiles * a.oh_tiles * a.n_tiles;
+  constexpr int kMT = 2;
+  a.pairs = (a.p_tiles + kMT - 1) / kMT;
+  a.stride = static_cast<uint32_t>(stride);
+  a.w_f = static_cast<uint32_t>(w_f);
+  a.c_slabs = static_cast<uint32_t>(c_slabs);
+  a.k_iters = static_cast<uint32_t>(h_f * stride * c_slabs);
+  if (bf16)
+    pack_filter_phase_kernel<true><<<256, 256, 0, stream>>>(flt, workspace, static_cast<int>(c_out),
+                                                            static_cast<int>(c_in), h_f, w_f, static_cast<int>(Mp),
+                                                            static_cast<int>(Kc));
+  else
+    pack_filter_phase_kernel<false><<<256, 256, 0, stream>>>(flt, workspace, static_cast<int>(c_out),
+                                                             static_cast<int>(c_in), h_f, w_f, static_cast<int>(Mp),
+                                                             static_cast<int>(Kc));
+  int rc = 1;
+  // stage = 2 x 17 KB of A + taps x N x 128 B of B; as many stages as fit in 227 KB
+#define IM2WIN_PH(BF, NN, ST, TP) \
+  rc = launch_phase<BF, NN, ST, TP, kMT>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err)
+#define IM2WIN_PH_T(BF)                                        \
+  switch (taps * 1000 + N) {                                   \
+    case 2064: IM2WIN_PH(BF, 64, 4, 2); break;                 \
+    case 2128: IM2WIN_PH(BF, 128, 3, 2); break;                \
+    case 3064: IM2WIN_PH(BF, 64, 3, 3); break;                 \
+    case 3128: IM2WIN_PH(BF, 128, 2, 3); break;                \
+    case 4064: IM2WIN_PH(BF, 64, 3, 4); break;                 \
+    case 4128: IM2WIN_PH(BF, 128, 2, 4); break;                \
+    case 5064: IM2WIN_PH(BF, 64, 3, 5); break;                 \
+    case 7064: IM2WIN_PH(BF, 64, 2, 7); break;                 \
+    default: break;                                            \
+  }
+  if (bf16) {
+    IM2WIN_PH_T(true)
+  } else {
+    IM2WIN_PH_T(false)
+  }
+#undef IM2WIN_PH_T
+#undef IM2WIN_PH
+  return rc == 0 ? 1 : -rc;
+}

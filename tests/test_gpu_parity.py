@@ -320,3 +320,37 @@ def test_host_pipeline_nonblocking_overlapped_submissions():
         jobs.append((h, ref))
     for h, ref in reversed(jobs):
         assert bits_equal(h.wait().numpy(), ref.numpy())
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+@pytest.mark.parametrize("select", ["phase", "shift", "generic"])
+def test_tc_kernel_selections_all_layers(select, variant, layer_goldens, monkeypatch):
+    """Each fused tensor-core kernel (phase-shift / window-shift / generic TMA window) is
+    within tolerance on every layer where it applies (forced through the library's env switches)."""
+    env = {"phase": ("2", "0"), "shift": ("0", "1"), "generic": ("0", "0")}[select]
+    monkeypatch.setenv("IM2WIN_PHASE", env[0])
+    monkeypatch.setenv("IM2WIN_SHIFT", env[1])
+    for name in BENCHMARKS:
+        g = layer_goldens[name]
+        cfg = replace(BENCHMARKS[name], batch=g["batch"], seed=g["seed"])
+        inp, flt = make_inputs(cfg)
+        ref = orc.conv_direct(inp, flt, cfg.stride)
+        out = pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant, tc_path="fused").numpy()
+        assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (name, select)
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_tc_phase_kernel_edge_geometries(variant, monkeypatch):
+    """Phase kernel on ragged geometries: odd/even H and W, stride 2 and 1, Wf 3/5/7, multi-row
+    tiles, an odd number of pixel tiles (the second tile of the last pair is empty)."""
+    monkeypatch.setenv("IM2WIN_PHASE", "2")
+    cases = [(3, 64, 17, 19, 64, 7, 7, 2), (2, 32, 30, 31, 96, 5, 5, 2), (1, 64, 23, 9, 64, 3, 3, 2),
+             (2, 40, 12, 13, 128, 3, 3, 1), (1, 64, 140, 140, 64, 7, 7, 2), (5, 32, 8, 8, 64, 5, 5, 1)]
+    for (n, c, h, w, co, hf, wf, s) in cases:
+        rng = np.random.default_rng(n * 1000 + h)
+        inp = rng.standard_normal((n, c, h, w), dtype=np.float32)
+        flt = rng.standard_normal((co, c, hf, wf), dtype=np.float32)
+        ref = orc.conv_direct(inp, flt, s)
+        out = pkg.conv_im2win_opt(inp, flt, pkg.ConvParams(c, co, hf, wf, s), variant=variant,
+                                  tc_path="fused").numpy()
+        assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (n, c, h, w, co, hf, wf, s)
