@@ -8,8 +8,8 @@
 // per (fh, phase, channel chunk) therefore feeds all ceil((Wf - r)/s) taps of that phase
 // through smem descriptors advanced by q rows (q * 128 B): A is fetched Wf/s times less
 // often than by the generic fused kernel (conv_tc_fused.cu), which fetches it per tap.
-// Each work item holds MT = 2 pixel tiles (two UMMA M=128 accumulators in TMEM) so every
-// staged filter tile feeds two MMAs: filter traffic from L2 halves as well.
+// Each work item holds MT = 2 or 4 pixel tiles (MT UMMA M=128 accumulators in TMEM) so every
+// staged filter tile feeds MT MMAs: filter traffic from L2 drops by MT as well.
 //
 //   A map (one per phase r): {c, j, fh % s, (oh*s + fh) / s, n} over the channels-last
 //     copy Xcl, strides {1, s*C, W*C, s*W*C, H*W*C} elements, base Xcl + r*C;
@@ -349,9 +349,10 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
   const char* env = getenv("IM2WIN_PHASE");
   const int mode = env ? atoi(env) : 1;  // 0: off, 1: auto, 2: force where legal (tests)
   if (mode == 0) return 0;
-  // measured (tools/tc_kernels.py, N=128): stride 2 (conv4) 1.35x over the generic fused
-  // kernel; at stride 1 the single-tile shift kernel (conv_tc_shift.cu) is as fast or faster
-  if (mode == 1 && stride == 1) return 0;
+  // measured (tools/tc_kernels.py, N=128): stride 2 (conv4, Co=64) 1.57x over the generic fused
+  // kernel; stride 1 with Co=64 (conv9, 4 tiles per item) 1.09x over the window-shift kernel;
+  // stride 1 with Co=128 (conv8, conv10): the shift kernel (conv_tc_shift.cu) is faster
+  if (mode == 1 && stride == 1 && c_out > 64) return 0;
   if (stride < 1 || stride > 2 || (w_f != 3 && w_f != 5 && w_f != 7) || c_out > 128) return 0;
   const int bk = bf16 ? 64 : 32;
   if (c_pad < 32) return 0;
@@ -380,8 +381,12 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
   a.oh_tiles = (a.h_out + a.rows - 1) / a.rows;
   a.n_tiles = (a.n_img + a.box_n - 1) / a.box_n;
   a.p_tiles = a.ow_tiles * a.oh_tiles * a.n_tiles;
-  constexpr int kMT = 2;
-  a.pairs = (a.p_tiles + kMT - 1) / kMT;
+  // pixel tiles per work item: every staged filter tile feeds mt MMAs.  Measured on conv4 BF16
+  // (N=128): 1 -> 570, 2 -> 724, 4 -> 835 TF; 4 tiles x 2 x 64 fp32 columns fill TMEM exactly.
+  const char* mt_env = getenv("IM2WIN_PHASE_MT");
+  int mt_sel = (N == 64 && taps <= 5) ? 4 : 2;
+  if (mt_env && (atoi(mt_env) == 2 || (atoi(mt_env) == 4 && N == 64 && taps <= 5))) mt_sel = atoi(mt_env);
+  a.pairs = (a.p_tiles + mt_sel - 1) / mt_sel;
   a.stride = static_cast<uint32_t>(stride);
   a.w_f = static_cast<uint32_t>(w_f);
   a.c_slabs = static_cast<uint32_t>(c_slabs);
@@ -397,7 +402,7 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
   int rc = 1;
   // stage = 2 x 17 KB of A + taps x N x 128 B of B; as many stages as fit in 227 KB
 #define IM2WIN_PH(BF, NN, ST, TP) \
-  rc = launch_phase<BF, NN, ST, TP, kMT>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err)
+  rc = launch_phase<BF, NN, ST, TP, 2>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err)
 #define IM2WIN_PH_T(BF)                                        \
   switch (taps * 1000 + N) {                                   \
     case 2064: IM2WIN_PH(BF, 64, 4, 2); break;                 \
@@ -410,7 +415,22 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
     case 7064: IM2WIN_PH(BF, 64, 2, 7); break;                 \
     default: break;                                            \
   }
-  if (bf16) {
+  if (mt_sel == 4) {
+    // stage = 4 x 17 KB of A + taps x 8 KB of B: two stages
+#define IM2WIN_PH4(BF)                                                                                   \
+  switch (taps) {                                                                                        \
+    case 2: rc = launch_phase<BF, 64, 2, 2, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err); break; \
+    case 3: rc = launch_phase<BF, 64, 2, 3, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err); break; \
+    case 4: rc = launch_phase<BF, 64, 2, 4, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err); break; \
+    default: rc = launch_phase<BF, 64, 2, 5, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err); break; \
+  }
+    if (bf16) {
+      IM2WIN_PH4(true)
+    } else {
+      IM2WIN_PH4(false)
+    }
+#undef IM2WIN_PH4
+  } else if (bf16) {
     IM2WIN_PH_T(true)
   } else {
     IM2WIN_PH_T(false)
