@@ -155,6 +155,10 @@ int im2win_bench_fp32_peak(float* sink, int32_t exact, int32_t iters, int32_t bl
 /* Message of the last failing call on this host thread ("" if none). */
 const char* im2win_last_error(void);
 
+/* Name of the compute kernel the last successful conv call on this host thread
+ * launched (which of the tile/kernel variants the library selected). */
+const char* im2win_last_kernel(void);
+
 /* ABI version of this library (major*100 + minor). */
 int32_t im2win_abi_version(void);
 

@@ -29,6 +29,7 @@ EXPORTED_SYMBOLS = (
     "im2win_conv_workspace_bytes",
     "im2win_conv_f32",
     "im2win_last_error",
+    "im2win_last_kernel",
     "im2win_abi_version",
     "im2win_bench_fp32_peak",
     "im2win_transform_cl",
@@ -82,6 +83,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         lib.im2win_conv_f32.restype = ctypes.c_int
         lib.im2win_last_error.argtypes = []
         lib.im2win_last_error.restype = ctypes.c_char_p
+        lib.im2win_last_kernel.argtypes = []
+        lib.im2win_last_kernel.restype = ctypes.c_char_p
         lib.im2win_abi_version.argtypes = []
         lib.im2win_abi_version.restype = ctypes.c_int32
         lib.im2win_bench_fp32_peak.argtypes = [vp, i32, i32, i32, vp]
@@ -114,6 +117,11 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         if path is None:
             _lib = lib
         return lib
+
+
+def last_kernel() -> str:
+    """Which kernel variant the last conv call on this thread launched (library-reported)."""
+    return load().im2win_last_kernel().decode()
 
 
 def check(rc: int) -> None:

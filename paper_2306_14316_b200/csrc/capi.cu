@@ -51,9 +51,14 @@ static int bind_device_of(const void* ptr) {
 
 int im2win_set_error(int code, const char* msg) { return fail(code, msg); }
 
+static thread_local const char* g_last_kernel = "";
+void im2win_note_kernel(const char* name) { g_last_kernel = name; }
+
 extern "C" {
 
 const char* im2win_last_error(void) { return g_last_error; }
+
+const char* im2win_last_kernel(void) { return g_last_kernel; }
 
 int32_t im2win_abi_version(void) { return 100; }
 

@@ -6,6 +6,10 @@
 
 #define IM2WIN_DEVICE __device__ __forceinline__
 
+// Records which kernel the last library call on this host thread launched
+// (im2win_last_kernel(); capi.cu).  Static strings only.
+void im2win_note_kernel(const char* name);
+
 namespace im2win {
 
 // Unsigned division by a runtime-invariant divisor via multiply-high

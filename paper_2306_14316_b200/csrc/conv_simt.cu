@@ -314,6 +314,7 @@ static cudaError_t launch_cfg(const ConvArgs& a0, cudaStream_t stream) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
+  im2win_note_kernel(MT == 8 ? "conv_simt_kernel (8x8 micro-tiles)" : "conv_simt_kernel (4x4 micro-tiles)");
   kern<<<static_cast<unsigned>(grid), (BM / MT) * (BN / MT), smem, stream>>>(a);
   return cudaGetLastError();
 }
@@ -536,6 +537,7 @@ int im2win_launch_conv_simt_1x1(const float* win, const float* flt, float* out, 
   a.fd_hw = FastDiv(static_cast<uint32_t>(hw)); a.fd_wo = FastDiv(static_cast<uint32_t>(w_out));
   a.m_tiles = (a.M + BM - 1) / BM;
   uint64_t grid = (static_cast<uint64_t>(n_gemm) + BN - 1) / BN * a.m_tiles;
+  im2win_note_kernel("conv_simt_1x1_kernel (TilePlan micro_kernel=False)");
   if (exact) {
     if (stages > 1) conv_simt_1x1_kernel<2, true><<<static_cast<unsigned>(grid), 256, 0, stream>>>(a);
     else conv_simt_1x1_kernel<1, true><<<static_cast<unsigned>(grid), 256, 0, stream>>>(a);
@@ -595,6 +597,7 @@ int im2win_launch_conv_basic(const float* win, const float* flt, float* out, int
     return 1;
   }
   dim3 grid(static_cast<unsigned>((n_gemm + 31) / 32), static_cast<unsigned>((c_out + 31) / 32));
+  im2win_note_kernel("conv_basic_kernel (paper Alg. 2)");
   conv_basic_kernel<<<grid, dim3(32, 32), 0, stream>>>(
       win, flt, out, static_cast<uint32_t>(n_gemm), static_cast<uint32_t>(c_out), static_cast<uint32_t>(K),
       static_cast<uint32_t>(c_in), static_cast<uint32_t>(h_out), static_cast<uint32_t>(row_len), h_f, w_f,

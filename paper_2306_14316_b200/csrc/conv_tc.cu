@@ -345,6 +345,7 @@ static int launch(const TcArgs& a0, void* packed, int Kp, int Mp, cudaStream_t s
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint32_t tiles = a.pix_tiles * a.co_tiles;
   const uint32_t grid = tiles < static_cast<uint32_t>(sms) ? tiles : static_cast<uint32_t>(sms);
+  im2win_note_kernel("conv_tc_kernel (gathered reference window tiles)");
   kern<<<grid, kThreads, smem, stream>>>(a, map);
   e = cudaGetLastError();
   if (e != cudaSuccess) {

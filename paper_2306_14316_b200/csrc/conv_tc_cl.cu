@@ -372,6 +372,7 @@ static int launch_cl(ClArgs a, const void* win_cl, const void* packed, int64_t K
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t tiles = static_cast<uint64_t>(a.g_tiles) * a.ow_tiles * a.co_tiles;
   const uint32_t grid = tiles < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(tiles) : static_cast<uint32_t>(sms);
+  im2win_note_kernel("conv_tc_cl_kernel (TMA over the channels-innermost window tensor)");
   kern<<<grid, 256, smem, stream>>>(a, map_a, map_b);
   e = cudaGetLastError();
   if (e != cudaSuccess) {

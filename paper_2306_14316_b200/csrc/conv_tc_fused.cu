@@ -61,6 +61,63 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restri
   }
 }
 
+// Wide-tile variant (c_pad > 8, Ho*Wo % 4 == 0): a CTA moves a 64-channel x 64-pixel
+// tile per iteration -- four 16-byte loads per thread in flight, a padded smem
+// transpose (row pitch 65 floats), and 16-byte channels-last stores (4 fp32 or 8 bf16
+// channels per store, the channel pitch is a multiple of that granule).
+template <bool BF16>
+__global__ void __launch_bounds__(256) nchw_to_nhwc_wide_kernel(const float* __restrict__ src, void* __restrict__ dst,
+                                                                uint32_t c_in, uint32_t c_pad, uint32_t hw,
+                                                                uint32_t hw_tiles, uint32_t c_tiles, uint32_t total) {
+  __shared__ float tile[64][65];
+  const uint32_t t = threadIdx.x;
+  for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
+    const uint32_t ct = b % c_tiles;
+    const uint32_t pt = (b / c_tiles) % hw_tiles;
+    const uint32_t img = b / (c_tiles * hw_tiles);
+    const uint32_t c0 = ct * 64, p0 = pt * 64;
+    const float* s = src + static_cast<uint64_t>(img) * c_in * hw;
+    // load: thread t covers pixels p0 + 4*(t%16) .. +3 of channels c0 + t/16 + 16*j
+    float4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t c = c0 + t / 16 + 16 * j, p = p0 + 4 * (t % 16);
+      v[j] = (c < c_in && p < hw) ? __ldcs(reinterpret_cast<const float4*>(s + static_cast<uint64_t>(c) * hw + p))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float* row = &tile[t / 16 + 16 * j][4 * (t % 16)];
+      row[0] = v[j].x; row[1] = v[j].y; row[2] = v[j].z; row[3] = v[j].w;
+    }
+    __syncthreads();
+    // store: 4 threads per pixel, 16 consecutive channels each
+    const uint32_t pl = t / 4, cq = t % 4;
+    const uint32_t p = p0 + pl;
+    if (p < hw) {
+      const uint64_t o = (static_cast<uint64_t>(img) * hw + p) * c_pad;
+#pragma unroll
+      for (int g = 0; g < 16; g += (BF16 ? 8 : 4)) {
+        const uint32_t cl = cq * 16 + g, c = c0 + cl;
+        if (c < c_pad) {
+          if constexpr (BF16) {
+            uint4 q;
+            q.x = pack_bf16x2(tile[cl][pl], tile[cl + 1][pl]);
+            q.y = pack_bf16x2(tile[cl + 2][pl], tile[cl + 3][pl]);
+            q.z = pack_bf16x2(tile[cl + 4][pl], tile[cl + 5][pl]);
+            q.w = pack_bf16x2(tile[cl + 6][pl], tile[cl + 7][pl]);
+            __stcs(reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dst) + o + c), q);
+          } else {
+            __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + o + c),
+                   make_float4(tile[cl][pl], tile[cl + 1][pl], tile[cl + 2][pl], tile[cl + 3][pl]));
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Few channels (c_pad <= 8, e.g. the RGB input layers): one thread per pixel reads its
 // C values (coalesced along the pixel axis) and writes the padded pixel with one
 // 16/32-byte store; the 32-channel smem transpose would leave most of its tile empty.
@@ -320,6 +377,7 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t tiles = static_cast<uint64_t>(a.n_tiles) * a.oh_tiles * a.ow_tiles * a.co_tiles;
   const uint32_t grid = tiles < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(tiles) : static_cast<uint32_t>(sms);
+  im2win_note_kernel(BF16 ? "conv_tc_fused_kernel (generic TMA window boxes, bf16)" : "conv_tc_fused_kernel (generic TMA window boxes, tf32)");
   kern<<<grid, kTcThreads, smem, stream>>>(a, map_a, map_b);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -363,6 +421,26 @@ int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c
       return 2;
     }
     return 0;
+  }
+  if (hw % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    const int64_t wt = n * ((hw + 63) / 64) * ((cp + 63) / 64);
+    if (wt < (1ll << 32)) {
+      const uint32_t g = static_cast<uint32_t>(std::min<int64_t>(wt, 148 * 8));
+      if (bf16)
+        im2win::tc::nchw_to_nhwc_wide_kernel<true><<<g, 256, 0, stream>>>(
+            src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(cp), static_cast<uint32_t>(hw),
+            static_cast<uint32_t>((hw + 63) / 64), static_cast<uint32_t>((cp + 63) / 64), static_cast<uint32_t>(wt));
+      else
+        im2win::tc::nchw_to_nhwc_wide_kernel<false><<<g, 256, 0, stream>>>(
+            src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(cp), static_cast<uint32_t>(hw),
+            static_cast<uint32_t>((hw + 63) / 64), static_cast<uint32_t>((cp + 63) / 64), static_cast<uint32_t>(wt));
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        *err = cudaGetErrorString(e);
+        return 2;
+      }
+      return 0;
+    }
   }
   const uint32_t grid = static_cast<uint32_t>(total < 148 * 16 ? total : 148 * 16);
   if (bf16)

@@ -303,6 +303,7 @@ static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t items = static_cast<uint64_t>(a.pairs) * a.co_tiles;
   const uint32_t grid = items < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(items) : static_cast<uint32_t>(sms);
+  im2win_note_kernel(MT == 4 ? "conv_tc_phase_kernel (phase shift, 4 tiles/item)" : "conv_tc_phase_kernel (phase shift, 2 tiles/item)");
   kern<<<grid, kTcThreads, smem, stream>>>(a, map_a[0], map_a[1], map_b);
   e = cudaGetLastError();
   if (e != cudaSuccess) {

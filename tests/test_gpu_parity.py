@@ -354,3 +354,24 @@ def test_tc_phase_kernel_edge_geometries(variant, monkeypatch):
         out = pkg.conv_im2win_opt(inp, flt, pkg.ConvParams(c, co, hf, wf, s), variant=variant,
                                   tc_path="fused").numpy()
         assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (n, c, h, w, co, hf, wf, s)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("shape", [(2, 3, 7, 9), (3, 64, 12, 12), (2, 96, 20, 20), (1, 130, 6, 10), (2, 40, 5, 5),
+                                   (1, 256, 14, 14)])
+def test_nhwc_copy_exact(shape, dtype):
+    """The channels-last copy feeding the fused TC kernels equals torch's permute (+ RN bf16
+    rounding) bit for bit, zero padded to the 16-byte channel pitch; every kernel shape."""
+    from paper_2306_14316_b200.kernels import nhwc_into, nhwc_pitch
+
+    g = torch.Generator(device="cpu").manual_seed(sum(shape))
+    x = torch.randn(shape, generator=g).to(DEV)
+    v = "bf16" if dtype == torch.bfloat16 else "tf32"
+    n, c, h, w = shape
+    cp = nhwc_pitch(c, v)
+    out = torch.full((n, h, w, cp), float("nan"), dtype=dtype, device=DEV)
+    nhwc_into(x, out)
+    ref = torch.zeros((n, h, w, cp), dtype=dtype, device=DEV)
+    ref[..., :c] = x.permute(0, 2, 3, 1).to(dtype)
+    assert torch.equal(out.view(torch.int16 if dtype == torch.bfloat16 else torch.int32),
+                       ref.view(torch.int16 if dtype == torch.bfloat16 else torch.int32))
