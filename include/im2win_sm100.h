@@ -63,6 +63,16 @@ typedef struct im2win_tile_plan {
 int im2win_transform_f32(const float* src, float* dst, int64_t n, int64_t c, int64_t h,
                          int64_t w, int32_t h_f, int32_t w_f, int32_t stride, void* stream);
 
+/* Extension: the same transform of the input zero-padded by `pad` on every side
+ * (the reference has no padding; callers pre-pad).  The padded input is never
+ * materialised: dst is (n, c, h_out, h_f * w_eff) for the padded geometry
+ * h_out = (h + 2*pad - h_f) / stride + 1, w_eff = (w_out - 1) * stride + w_f,
+ * bit-identical to im2win_transform_f32 of the explicitly padded input.
+ * src and dst must be 16-byte aligned when pad > 0. */
+int im2win_transform_f32_padded(const float* src, float* dst, int64_t n, int64_t c, int64_t h,
+                                int64_t w, int32_t h_f, int32_t w_f, int32_t stride, int32_t pad,
+                                void* stream);
+
 /* Bytes of device workspace im2win_conv_f32 needs (packed filter + offsets). */
 size_t im2win_conv_workspace_bytes(int64_t c_in, int64_t c_out, int32_t h_f, int32_t w_f,
                                    int32_t variant);
@@ -107,6 +117,12 @@ int im2win_conv_cl(const void* windows_cl, const float* flt, float* out, int64_t
 int im2win_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w,
                         int32_t dtype, void* stream);
 
+/* The same copy into a spatially zero-padded destination (n, h + 2*pad, w + 2*pad,
+ * pitch): border pixels are written as zeros, so im2win_conv_fused on it with the
+ * padded extents computes the padded convolution. */
+int im2win_nchw_to_nhwc_padded(const float* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w,
+                               int32_t dtype, int32_t pad, void* stream);
+
 size_t im2win_conv_fused_workspace_bytes(int64_t c_in, int64_t c_out, int32_t h_f, int32_t w_f);
 
 int im2win_conv_fused(const void* x_nhwc, const float* flt, float* out, int64_t n, int64_t c_in,
@@ -118,19 +134,20 @@ int im2win_conv_fused(const void* x_nhwc, const float* flt, float* out, int64_t 
  * This runs transform + conv over host buffers: the batch is cut into chunks of
  * chunk_images (<= 0: about n/8) and a three-stream pipeline overlaps the
  * upload of chunk k+1, the kernels of chunk k and the download of chunk k-1.
- * host_in (n,c_in,h,w), host_flt (c_out,c_in,h_f,w_f), host_out (n,c_out,h_out,w_out)
+ * host_in (n,c_in,h,w), host_flt (c_out,c_in,h_f,w_f), host_out (n,c_out,h_out,w_out);
+ * pad >= 0 zero-pads the input on every side (0 = the reference's unpadded conv)
  * are host memory (page-locked for overlap); workspace is device memory of at
  * least im2win_conv_host_workspace_bytes(...) bytes on the device to run on.
  * Ordered after prior work on `stream`; blocks until host_out is written.
  * Results are bit-identical to im2win_transform_f32 + im2win_conv_f32
  * (FP32 variants) or im2win_nchw_to_nhwc + im2win_conv_fused (TF32/BF16). */
 size_t im2win_conv_host_workspace_bytes(int64_t n, int64_t c_in, int64_t h, int64_t w, int64_t c_out,
-                                        int32_t h_f, int32_t w_f, int32_t stride, int32_t variant,
-                                        int64_t chunk_images);
+                                        int32_t h_f, int32_t w_f, int32_t stride, int32_t pad,
+                                        int32_t variant, int64_t chunk_images);
 
 int im2win_conv_host_f32(const float* host_in, const float* host_flt, float* host_out, int64_t n,
                          int64_t c_in, int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f,
-                         int32_t stride, const im2win_tile_plan* plan, int32_t variant,
+                         int32_t stride, int32_t pad, const im2win_tile_plan* plan, int32_t variant,
                          int64_t chunk_images, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Non-blocking form: enqueues the same work and returns at once with a ticket;
@@ -140,7 +157,7 @@ int im2win_conv_host_f32(const float* host_in, const float* host_flt, float* hos
  * previous).  The caller's stream is only used to order the start. */
 int im2win_conv_host_submit(const float* host_in, const float* host_flt, float* host_out, int64_t n,
                             int64_t c_in, int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f,
-                            int32_t stride, const im2win_tile_plan* plan, int32_t variant,
+                            int32_t stride, int32_t pad, const im2win_tile_plan* plan, int32_t variant,
                             int64_t chunk_images, void* workspace, size_t workspace_bytes, void* stream,
                             int64_t* ticket);
 

@@ -26,6 +26,7 @@ VARIANTS = {"fp32-exact": FP32_EXACT, "fp32-fma": FP32_FMA, "tf32": TF32, "bf16"
 # every symbol include/im2win_sm100.h declares
 EXPORTED_SYMBOLS = (
     "im2win_transform_f32",
+    "im2win_transform_f32_padded",
     "im2win_conv_workspace_bytes",
     "im2win_conv_f32",
     "im2win_last_error",
@@ -36,6 +37,7 @@ EXPORTED_SYMBOLS = (
     "im2win_conv_cl_workspace_bytes",
     "im2win_conv_cl",
     "im2win_nchw_to_nhwc",
+    "im2win_nchw_to_nhwc_padded",
     "im2win_conv_fused_workspace_bytes",
     "im2win_conv_fused",
     "im2win_conv_basic_f32",
@@ -76,6 +78,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         i64, i32, vp, sz = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t
         lib.im2win_transform_f32.argtypes = [vp, vp, i64, i64, i64, i64, i32, i32, i32, vp]
         lib.im2win_transform_f32.restype = ctypes.c_int
+        lib.im2win_transform_f32_padded.argtypes = [vp, vp, i64, i64, i64, i64, i32, i32, i32, i32, vp]
+        lib.im2win_transform_f32_padded.restype = ctypes.c_int
         lib.im2win_conv_workspace_bytes.argtypes = [i64, i64, i32, i32, i32]
         lib.im2win_conv_workspace_bytes.restype = sz
         lib.im2win_conv_f32.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i32, i32, i32,
@@ -97,18 +101,20 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         lib.im2win_conv_cl.restype = ctypes.c_int
         lib.im2win_nchw_to_nhwc.argtypes = [vp, vp, i64, i64, i64, i64, i32, vp]
         lib.im2win_nchw_to_nhwc.restype = ctypes.c_int
+        lib.im2win_nchw_to_nhwc_padded.argtypes = [vp, vp, i64, i64, i64, i64, i32, i32, vp]
+        lib.im2win_nchw_to_nhwc_padded.restype = ctypes.c_int
         lib.im2win_conv_fused_workspace_bytes.argtypes = [i64, i64, i32, i32]
         lib.im2win_conv_fused_workspace_bytes.restype = sz
         lib.im2win_conv_fused.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32, i32, vp, sz, vp]
         lib.im2win_conv_fused.restype = ctypes.c_int
         lib.im2win_conv_basic_f32.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i32, i32, i32, vp]
         lib.im2win_conv_basic_f32.restype = ctypes.c_int
-        lib.im2win_conv_host_workspace_bytes.argtypes = [i64, i64, i64, i64, i64, i32, i32, i32, i32, i64]
+        lib.im2win_conv_host_workspace_bytes.argtypes = [i64, i64, i64, i64, i64, i32, i32, i32, i32, i32, i64]
         lib.im2win_conv_host_workspace_bytes.restype = sz
-        lib.im2win_conv_host_f32.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32,
+        lib.im2win_conv_host_f32.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32, i32,
                                              ctypes.POINTER(TilePlanC), i32, i64, vp, sz, vp]
         lib.im2win_conv_host_f32.restype = ctypes.c_int
-        lib.im2win_conv_host_submit.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32,
+        lib.im2win_conv_host_submit.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32, i32,
                                                 ctypes.POINTER(TilePlanC), i32, i64, vp, sz, vp,
                                                 ctypes.POINTER(ctypes.c_int64)]
         lib.im2win_conv_host_submit.restype = ctypes.c_int

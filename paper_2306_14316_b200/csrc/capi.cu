@@ -7,7 +7,7 @@
 #include "../../include/im2win_sm100.h"
 
 int im2win_launch_transform(const float* src, float* dst, int64_t n, int64_t c, int64_t h, int64_t w,
-                            int h_f, int w_f, int stride, int64_t h_out, int64_t w_eff,
+                            int h_f, int w_f, int stride, int64_t h_out, int64_t w_eff, int pad,
                             cudaStream_t stream, const char** err);
 int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void* workspace,
                             int64_t n, int64_t c_in, int64_t c_out, int64_t h_out, int64_t w_out,
@@ -62,21 +62,26 @@ const char* im2win_last_kernel(void) { return g_last_kernel; }
 
 int32_t im2win_abi_version(void) { return 100; }
 
-int im2win_transform_f32(const float* src, float* dst, int64_t n, int64_t c, int64_t h, int64_t w,
-                         int32_t h_f, int32_t w_f, int32_t stride, void* stream) {
+int im2win_transform_f32_padded(const float* src, float* dst, int64_t n, int64_t c, int64_t h, int64_t w,
+                                int32_t h_f, int32_t w_f, int32_t stride, int32_t pad, void* stream) {
   g_last_error[0] = '\0';
   if (!src || !dst) return fail(1, "im2win_transform_f32: null pointer");
-  if (n < 1 || c < 1 || h < 1 || w < 1 || h_f < 1 || w_f < 1 || stride < 1)
-    return fail(1, "im2win_transform_f32: extents must be positive");
-  if (h_f > h || w_f > w) return fail(1, "im2win_transform_f32: filter larger than input");
+  if (n < 1 || c < 1 || h < 1 || w < 1 || h_f < 1 || w_f < 1 || stride < 1 || pad < 0)
+    return fail(1, "im2win_transform_f32: extents must be positive (pad >= 0)");
+  if (h_f > h + 2 * pad || w_f > w + 2 * pad) return fail(1, "im2win_transform_f32: filter larger than input");
   if (int rc = bind_device_of(dst)) return rc;
-  const int64_t h_out = (h - h_f) / stride + 1;
-  const int64_t w_out = (w - w_f) / stride + 1;
+  const int64_t h_out = (h + 2 * pad - h_f) / stride + 1;
+  const int64_t w_out = (w + 2 * pad - w_f) / stride + 1;
   const int64_t w_eff = (w_out - 1) * stride + w_f;
   const char* err = nullptr;
-  int rc = im2win_launch_transform(src, dst, n, c, h, w, h_f, w_f, stride, h_out, w_eff,
+  int rc = im2win_launch_transform(src, dst, n, c, h, w, h_f, w_f, stride, h_out, w_eff, pad,
                                    static_cast<cudaStream_t>(stream), &err);
   return rc ? fail(rc, err) : 0;
+}
+
+int im2win_transform_f32(const float* src, float* dst, int64_t n, int64_t c, int64_t h, int64_t w,
+                         int32_t h_f, int32_t w_f, int32_t stride, void* stream) {
+  return im2win_transform_f32_padded(src, dst, n, c, h, w, h_f, w_f, stride, 0, stream);
 }
 
 size_t im2win_conv_workspace_bytes(int64_t c_in, int64_t c_out, int32_t h_f, int32_t w_f,
@@ -182,7 +187,7 @@ int im2win_conv_cl(const void* windows_cl, const float* flt, float* out, int64_t
 
 // ---- fused tensor-core path: TMA window view over an NHWC copy (conv_tc_fused.cu) ----
 int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w, int bf16,
-                               cudaStream_t stream, const char** err);
+                               int pad, cudaStream_t stream, const char** err);
 size_t im2win_tc_fused_workspace_bytes(int64_t c_in, int64_t c_out, int h_f, int w_f);
 int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n,
                                 int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride,
@@ -190,16 +195,23 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
 
 extern "C" {
 
-int im2win_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w, int32_t dtype,
-                        void* stream) {
+int im2win_nchw_to_nhwc_padded(const float* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w, int32_t dtype,
+                               int32_t pad, void* stream) {
   g_last_error[0] = '\0';
   if (!src || !dst) return fail(1, "im2win_nchw_to_nhwc: null pointer");
-  if (n < 1 || c < 1 || h < 1 || w < 1) return fail(1, "im2win_nchw_to_nhwc: extents must be positive");
+  if (n < 1 || c < 1 || h < 1 || w < 1 || pad < 0) return fail(1, "im2win_nchw_to_nhwc: extents must be positive");
   if (dtype != 0 && dtype != 1) return fail(1, "im2win_nchw_to_nhwc: dtype must be 0 (f32) or 1 (bf16)");
+  if (pad > 0 && (reinterpret_cast<uintptr_t>(dst) & 15) != 0)
+    return fail(1, "im2win_nchw_to_nhwc: a padded copy needs a 16-byte aligned destination");
   if (int rc = bind_device_of(dst)) return rc;
   const char* err = nullptr;
-  int rc = im2win_launch_nchw_to_nhwc(src, dst, n, c, h, w, dtype, static_cast<cudaStream_t>(stream), &err);
+  int rc = im2win_launch_nchw_to_nhwc(src, dst, n, c, h, w, dtype, pad, static_cast<cudaStream_t>(stream), &err);
   return rc ? fail(rc, err) : 0;
+}
+
+int im2win_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w, int32_t dtype,
+                        void* stream) {
+  return im2win_nchw_to_nhwc_padded(src, dst, n, c, h, w, dtype, 0, stream);
 }
 
 size_t im2win_conv_fused_workspace_bytes(int64_t c_in, int64_t c_out, int32_t h_f, int32_t w_f) {

@@ -22,12 +22,27 @@
 namespace im2win {
 namespace tc {
 
+// Destination pixel index of source pixel p (row-major in an h x w image) in a
+// channels-last copy whose spatial extent is zero-padded by `pad` on every side.
+struct PadMap {
+  uint32_t pad, wp;   // wp = w + 2*pad
+  uint64_t img_px;    // (h + 2*pad) * wp pixels per image
+  FastDiv fd_w;
+  IM2WIN_DEVICE uint64_t pixel(uint64_t img, uint32_t p) const {
+    if (pad == 0) return img * img_px + p;
+    uint32_t y, x;
+    fd_w.divmod(p, y, x);
+    return img * img_px + static_cast<uint64_t>(y + pad) * wp + x + pad;
+  }
+};
+
 // NCHW float32 -> NHWC (float32 or bf16) with the channel pitch padded to c_pad
 // (a 16-byte multiple, zero filled): per image a [C][H*W] -> [H*W][c_pad] transpose.
 template <bool BF16>
 __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restrict__ src, void* __restrict__ dst,
                                                            uint32_t c_in, uint32_t c_pad, uint32_t hw,
-                                                           uint32_t hw_tiles, uint32_t c_tiles, uint32_t total) {
+                                                           uint32_t hw_tiles, uint32_t c_tiles, uint32_t total,
+                                                           const PadMap pm) {
   __shared__ float tile[32][33];
   const uint32_t tx = threadIdx.x % 32, ty = threadIdx.x / 32;
   for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
@@ -47,7 +62,7 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restri
     const uint32_t p = p0 + pl, c = c0 + cq * 4;
     if (p < hw && c < c_pad) {
       const float v0 = tile[cq * 4][pl], v1 = tile[cq * 4 + 1][pl], v2 = tile[cq * 4 + 2][pl], v3 = tile[cq * 4 + 3][pl];
-      const uint64_t o = (static_cast<uint64_t>(img) * hw + p) * c_pad + c;
+      const uint64_t o = pm.pixel(img, p) * c_pad + c;
       if constexpr (BF16) {
         uint2 q;
         q.x = pack_bf16x2(v0, v1);
@@ -68,7 +83,8 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restri
 template <bool BF16>
 __global__ void __launch_bounds__(256) nchw_to_nhwc_wide_kernel(const float* __restrict__ src, void* __restrict__ dst,
                                                                 uint32_t c_in, uint32_t c_pad, uint32_t hw,
-                                                                uint32_t hw_tiles, uint32_t c_tiles, uint32_t total) {
+                                                                uint32_t hw_tiles, uint32_t c_tiles, uint32_t total,
+                                                                const PadMap pm) {
   __shared__ float tile[64][65];
   const uint32_t t = threadIdx.x;
   for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
@@ -95,7 +111,7 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_wide_kernel(const float* __r
     const uint32_t pl = t / 4, cq = t % 4;
     const uint32_t p = p0 + pl;
     if (p < hw) {
-      const uint64_t o = (static_cast<uint64_t>(img) * hw + p) * c_pad;
+      const uint64_t o = pm.pixel(img, p) * c_pad;
 #pragma unroll
       for (int g = 0; g < 16; g += (BF16 ? 8 : 4)) {
         const uint32_t cl = cq * 16 + g, c = c0 + cl;
@@ -124,11 +140,12 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_wide_kernel(const float* __r
 template <bool BF16>
 __global__ void __launch_bounds__(256) nchw_to_nhwc_small_kernel(const float* __restrict__ src, void* __restrict__ dst,
                                                                  uint32_t c_in, uint32_t c_pad, uint64_t hw,
-                                                                 uint64_t total) {
+                                                                 uint64_t total, const PadMap pm) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t img = i / hw, p = i % hw;
     const float* s = src + img * c_in * hw + p;
+    const uint64_t od = pm.pixel(img, static_cast<uint32_t>(p));
     float v[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) v[c] = (static_cast<uint32_t>(c) < c_in) ? __ldg(s + c * hw) : 0.0f;
@@ -139,12 +156,24 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_small_kernel(const float* __
       q.y = pack_bf16x2(v[2], v[3]);
       q.z = pack_bf16x2(v[4], v[5]);
       q.w = pack_bf16x2(v[6], v[7]);
-      reinterpret_cast<uint4*>(dst)[i] = q;
+      reinterpret_cast<uint4*>(dst)[od] = q;
     } else {
-      float4* d = reinterpret_cast<float4*>(dst) + i * (c_pad / 4);
+      float4* d = reinterpret_cast<float4*>(dst) + od * (c_pad / 4);
       d[0] = make_float4(v[0], v[1], v[2], v[3]);
       if (c_pad == 8) d[1] = make_float4(v[4], v[5], v[6], v[7]);
     }
+  }
+}
+
+// Zero the border pixels (all c_pad channels) of a spatially padded channels-last copy.
+__global__ void __launch_bounds__(256) nhwc_zero_border_kernel(uint4* __restrict__ dst, uint32_t vec_per_px,
+                                                               uint32_t hp, uint32_t wp, uint32_t pad,
+                                                               uint64_t total_px) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total_px * vec_per_px;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t px = i / vec_per_px;
+    const uint32_t x = static_cast<uint32_t>(px % wp), y = static_cast<uint32_t>((px / wp) % hp);
+    if (y < pad || y >= hp - pad || x < pad || x >= wp - pad) dst[i] = make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -397,30 +426,49 @@ int64_t im2win_nhwc_channel_pitch(int64_t c, int bf16) {
 }
 
 int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w, int bf16,
-                               cudaStream_t stream, const char** err) {
+                               int pad, cudaStream_t stream, const char** err) {
+  using im2win::tc::PadMap;
   const int64_t hw = h * w;
   const int64_t cp = im2win_nhwc_channel_pitch(c, bf16);
   const int64_t hw_tiles = (hw + 31) / 32, c_tiles = (cp + 31) / 32;
   const int64_t total = n * hw_tiles * c_tiles;
-  if (total >= (1ll << 32) || hw >= (1ll << 31)) {
+  const int64_t hp = h + 2 * pad, wp = w + 2 * pad;
+  if (total >= (1ll << 32) || hw >= (1ll << 31) || hp * wp >= (1ll << 31)) {
     *err = "nchw_to_nhwc: extents exceed the kernel's index range";
     return 1;
   }
-  if (cp <= 8) {
-    const uint64_t pixels = static_cast<uint64_t>(n) * hw;
-    const uint32_t g = static_cast<uint32_t>(std::min<uint64_t>((pixels + 255) / 256, 148 * 32));
-    if (bf16)
-      im2win::tc::nchw_to_nhwc_small_kernel<true><<<g, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
-                                                                         static_cast<uint32_t>(cp), hw, pixels);
-    else
-      im2win::tc::nchw_to_nhwc_small_kernel<false><<<g, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
-                                                                          static_cast<uint32_t>(cp), hw, pixels);
+  PadMap pm;
+  pm.pad = static_cast<uint32_t>(pad);
+  pm.wp = static_cast<uint32_t>(wp);
+  pm.img_px = static_cast<uint64_t>(hp * wp);
+  pm.fd_w = im2win::FastDiv(static_cast<uint32_t>(w));
+  auto done = [&]() -> int {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       *err = cudaGetErrorString(e);
       return 2;
     }
     return 0;
+  };
+  if (pad > 0) {
+    // border pixels: zeros across the whole channel pitch (cp * esz is a 16-byte multiple)
+    const uint32_t vec = static_cast<uint32_t>(cp * (bf16 ? 2 : 4) / 16);
+    const uint64_t px = static_cast<uint64_t>(n) * hp * wp;
+    const uint32_t g = static_cast<uint32_t>(std::min<uint64_t>((px * vec + 255) / 256, 148 * 16));
+    im2win::tc::nhwc_zero_border_kernel<<<g, 256, 0, stream>>>(static_cast<uint4*>(dst), vec,
+                                                               static_cast<uint32_t>(hp), static_cast<uint32_t>(wp),
+                                                               static_cast<uint32_t>(pad), px);
+  }
+  if (cp <= 8) {
+    const uint64_t pixels = static_cast<uint64_t>(n) * hw;
+    const uint32_t g = static_cast<uint32_t>(std::min<uint64_t>((pixels + 255) / 256, 148 * 32));
+    if (bf16)
+      im2win::tc::nchw_to_nhwc_small_kernel<true><<<g, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
+                                                                         static_cast<uint32_t>(cp), hw, pixels, pm);
+    else
+      im2win::tc::nchw_to_nhwc_small_kernel<false><<<g, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
+                                                                          static_cast<uint32_t>(cp), hw, pixels, pm);
+    return done();
   }
   if (hw % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
     const int64_t wt = n * ((hw + 63) / 64) * ((cp + 63) / 64);
@@ -429,40 +477,24 @@ int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c
       if (bf16)
         im2win::tc::nchw_to_nhwc_wide_kernel<true><<<g, 256, 0, stream>>>(
             src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(cp), static_cast<uint32_t>(hw),
-            static_cast<uint32_t>((hw + 63) / 64), static_cast<uint32_t>((cp + 63) / 64), static_cast<uint32_t>(wt));
+            static_cast<uint32_t>((hw + 63) / 64), static_cast<uint32_t>((cp + 63) / 64), static_cast<uint32_t>(wt), pm);
       else
         im2win::tc::nchw_to_nhwc_wide_kernel<false><<<g, 256, 0, stream>>>(
             src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(cp), static_cast<uint32_t>(hw),
-            static_cast<uint32_t>((hw + 63) / 64), static_cast<uint32_t>((cp + 63) / 64), static_cast<uint32_t>(wt));
-      cudaError_t e = cudaGetLastError();
-      if (e != cudaSuccess) {
-        *err = cudaGetErrorString(e);
-        return 2;
-      }
-      return 0;
+            static_cast<uint32_t>((hw + 63) / 64), static_cast<uint32_t>((cp + 63) / 64), static_cast<uint32_t>(wt), pm);
+      return done();
     }
   }
   const uint32_t grid = static_cast<uint32_t>(total < 148 * 16 ? total : 148 * 16);
   if (bf16)
-    im2win::tc::nchw_to_nhwc_kernel<true><<<grid, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
-                                                                     static_cast<uint32_t>(cp),
-                                                                     static_cast<uint32_t>(hw),
-                                                                     static_cast<uint32_t>(hw_tiles),
-                                                                     static_cast<uint32_t>(c_tiles),
-                                                                     static_cast<uint32_t>(total));
+    im2win::tc::nchw_to_nhwc_kernel<true><<<grid, 256, 0, stream>>>(
+        src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(cp), static_cast<uint32_t>(hw),
+        static_cast<uint32_t>(hw_tiles), static_cast<uint32_t>(c_tiles), static_cast<uint32_t>(total), pm);
   else
-    im2win::tc::nchw_to_nhwc_kernel<false><<<grid, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
-                                                                      static_cast<uint32_t>(cp),
-                                                                      static_cast<uint32_t>(hw),
-                                                                      static_cast<uint32_t>(hw_tiles),
-                                                                      static_cast<uint32_t>(c_tiles),
-                                                                      static_cast<uint32_t>(total));
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    *err = cudaGetErrorString(e);
-    return 2;
-  }
-  return 0;
+    im2win::tc::nchw_to_nhwc_kernel<false><<<grid, 256, 0, stream>>>(
+        src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(cp), static_cast<uint32_t>(hw),
+        static_cast<uint32_t>(hw_tiles), static_cast<uint32_t>(c_tiles), static_cast<uint32_t>(total), pm);
+  return done();
 }
 
 size_t im2win_tc_fused_workspace_bytes(int64_t c_in, int64_t c_out, int h_f, int w_f) {

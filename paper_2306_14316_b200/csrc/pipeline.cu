@@ -50,7 +50,7 @@ DevPipe g_pipes[kMaxDev];
 
 struct Geometry {
   int64_t n, c_in, h, w, c_out, h_out, w_out, w_eff;
-  int h_f, w_f, stride;
+  int h_f, w_f, stride, pad;
   bool tc;
   int64_t pitch;  // channels-last pitch for the TC path
   size_t in_elems, mid_bytes, out_elems, flt_elems, conv_ws;
@@ -59,7 +59,7 @@ struct Geometry {
 size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 Geometry geometry(int64_t n_chunk, int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride,
-                  int variant) {
+                  int pad, int variant) {
   Geometry g{};
   g.n = n_chunk;
   g.c_in = c_in;
@@ -69,8 +69,9 @@ Geometry geometry(int64_t n_chunk, int64_t c_in, int64_t h, int64_t w, int64_t c
   g.h_f = h_f;
   g.w_f = w_f;
   g.stride = stride;
-  g.h_out = (h - h_f) / stride + 1;
-  g.w_out = (w - w_f) / stride + 1;
+  g.pad = pad;
+  g.h_out = (h + 2 * pad - h_f) / stride + 1;
+  g.w_out = (w + 2 * pad - w_f) / stride + 1;
   g.w_eff = (g.w_out - 1) * stride + w_f;
   g.tc = variant == IM2WIN_TF32 || variant == IM2WIN_BF16;
   const int q = variant == IM2WIN_BF16 ? 8 : 4;
@@ -79,7 +80,7 @@ Geometry geometry(int64_t n_chunk, int64_t c_in, int64_t h, int64_t w, int64_t c
   g.out_elems = static_cast<size_t>(n_chunk * c_out * g.h_out * g.w_out);
   g.flt_elems = static_cast<size_t>(c_out * c_in * h_f * w_f);
   if (g.tc) {
-    g.mid_bytes = static_cast<size_t>(n_chunk * h * w * g.pitch) * (variant == IM2WIN_BF16 ? 2 : 4);
+    g.mid_bytes = static_cast<size_t>(n_chunk * (h + 2 * pad) * (w + 2 * pad) * g.pitch) * (variant == IM2WIN_BF16 ? 2 : 4);
     g.conv_ws = im2win_conv_fused_workspace_bytes(c_in, c_out, h_f, w_f);
   } else {
     g.mid_bytes = static_cast<size_t>(n_chunk * c_in * g.h_out * h_f * g.w_eff) * 4;
@@ -114,27 +115,30 @@ int64_t pick_chunk(int64_t n, int64_t chunk) {
 extern "C" {
 
 size_t im2win_conv_host_workspace_bytes(int64_t n, int64_t c_in, int64_t h, int64_t w, int64_t c_out, int32_t h_f,
-                                        int32_t w_f, int32_t stride, int32_t variant, int64_t chunk_images) {
-  if (n < 1 || c_in < 1 || h < 1 || w < 1 || c_out < 1 || h_f < 1 || w_f < 1 || stride < 1 || h_f > h || w_f > w)
+                                        int32_t w_f, int32_t stride, int32_t pad, int32_t variant,
+                                        int64_t chunk_images) {
+  if (n < 1 || c_in < 1 || h < 1 || w < 1 || c_out < 1 || h_f < 1 || w_f < 1 || stride < 1 || pad < 0 ||
+      h_f > h + 2 * pad || w_f > w + 2 * pad)
     return 0;
   const int64_t cn = pick_chunk(n, chunk_images);
-  return workspace_bytes(geometry(cn, c_in, h, w, c_out, h_f, w_f, stride, variant));
+  return workspace_bytes(geometry(cn, c_in, h, w, c_out, h_f, w_f, stride, pad, variant));
 }
 
 }  // extern "C"
 
 static int host_conv(const float* host_in, const float* host_flt, float* host_out, int64_t n, int64_t c_in,
-                     int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
+                     int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride, int32_t pad,
                      const im2win_tile_plan* plan, int32_t variant, int64_t chunk_images, void* workspace,
                      size_t ws_bytes, void* stream, int64_t* ticket) {
   if (!host_in || !host_flt || !host_out || !workspace) return im2win_set_error(1, "im2win_conv_host_f32: null pointer");
-  if (n < 1 || c_in < 1 || h < 1 || w < 1 || c_out < 1 || h_f < 1 || w_f < 1 || stride < 1)
+  if (n < 1 || c_in < 1 || h < 1 || w < 1 || c_out < 1 || h_f < 1 || w_f < 1 || stride < 1 || pad < 0)
     return im2win_set_error(1, "im2win_conv_host_f32: extents must be positive");
-  if (h_f > h || w_f > w) return im2win_set_error(1, "im2win_conv_host_f32: filter larger than input");
+  if (h_f > h + 2 * pad || w_f > w + 2 * pad)
+    return im2win_set_error(1, "im2win_conv_host_f32: filter larger than input");
   if (variant < IM2WIN_FP32_EXACT || variant > IM2WIN_BF16)
     return im2win_set_error(1, "im2win_conv_host_f32: unknown variant");
   const int64_t cn = pick_chunk(n, chunk_images);
-  const Geometry g = geometry(cn, c_in, h, w, c_out, h_f, w_f, stride, variant);
+  const Geometry g = geometry(cn, c_in, h, w, c_out, h_f, w_f, stride, pad, variant);
   if (ws_bytes < workspace_bytes(g)) return im2win_set_error(1, "im2win_conv_host_f32: workspace too small");
 
   cudaPointerAttributes attr;
@@ -204,13 +208,14 @@ static int host_conv(const float* host_in, const float* host_flt, float* host_ou
     cudaStreamWaitEvent(P.comp, P.in_ready[s], 0);
     if (k >= D) cudaStreamWaitEvent(P.comp, P.out_done[s], 0);
     if (g.tc) {
-      rc = im2win_nchw_to_nhwc(d_in[s], mid, nk, c_in, h, w, variant == IM2WIN_BF16 ? 1 : 0, P.comp);
+      rc = im2win_nchw_to_nhwc_padded(d_in[s], mid, nk, c_in, h, w, variant == IM2WIN_BF16 ? 1 : 0, pad, P.comp);
       cudaEventRecord(P.xf_done[s], P.comp);
       if (!rc)
-        rc = im2win_conv_fused(mid, d_flt, d_out[s], nk, c_in, h, w, c_out, h_f, w_f, stride, variant, conv_ws,
-                               g.conv_ws, P.comp);
+        rc = im2win_conv_fused(mid, d_flt, d_out[s], nk, c_in, h + 2 * pad, w + 2 * pad, c_out, h_f, w_f, stride,
+                               variant, conv_ws, g.conv_ws, P.comp);
     } else {
-      rc = im2win_transform_f32(d_in[s], static_cast<float*>(mid), nk, c_in, h, w, h_f, w_f, stride, P.comp);
+      rc = im2win_transform_f32_padded(d_in[s], static_cast<float*>(mid), nk, c_in, h, w, h_f, w_f, stride, pad,
+                                       P.comp);
       cudaEventRecord(P.xf_done[s], P.comp);
       if (!rc)
         rc = im2win_conv_f32(static_cast<float*>(mid), d_flt, d_out[s], nk, c_in, c_out, g.h_out, g.w_out,
@@ -248,20 +253,20 @@ static int host_conv(const float* host_in, const float* host_flt, float* host_ou
 extern "C" {
 
 int im2win_conv_host_f32(const float* host_in, const float* host_flt, float* host_out, int64_t n, int64_t c_in,
-                         int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
+                         int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride, int32_t pad,
                          const im2win_tile_plan* plan, int32_t variant, int64_t chunk_images, void* workspace,
                          size_t ws_bytes, void* stream) {
-  return host_conv(host_in, host_flt, host_out, n, c_in, h, w, c_out, h_f, w_f, stride, plan, variant, chunk_images,
-                   workspace, ws_bytes, stream, nullptr);
+  return host_conv(host_in, host_flt, host_out, n, c_in, h, w, c_out, h_f, w_f, stride, pad, plan, variant,
+                   chunk_images, workspace, ws_bytes, stream, nullptr);
 }
 
 int im2win_conv_host_submit(const float* host_in, const float* host_flt, float* host_out, int64_t n, int64_t c_in,
-                            int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
+                            int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride, int32_t pad,
                             const im2win_tile_plan* plan, int32_t variant, int64_t chunk_images, void* workspace,
                             size_t ws_bytes, void* stream, int64_t* ticket) {
   if (!ticket) return im2win_set_error(1, "im2win_conv_host_submit: null ticket");
-  return host_conv(host_in, host_flt, host_out, n, c_in, h, w, c_out, h_f, w_f, stride, plan, variant, chunk_images,
-                   workspace, ws_bytes, stream, ticket);
+  return host_conv(host_in, host_flt, host_out, n, c_in, h, w, c_out, h_f, w_f, stride, pad, plan, variant,
+                   chunk_images, workspace, ws_bytes, stream, ticket);
 }
 
 int im2win_conv_host_wait(int64_t ticket) {

@@ -26,6 +26,7 @@ struct TransformArgs {
   uint32_t tile_floats; // staged-input capacity (floats, multiple of 4)
   uint32_t rows_per_cta;
   FastDiv fd_ho, fd_rl, fd_hf, fd_weff;
+  uint32_t pad;         // zero padding on every side (pipelined kernel only); h_out/w_eff are padded geometry
 };
 
 IM2WIN_DEVICE uint64_t in_row_of(const TransformArgs& a, uint32_t g) {
@@ -149,18 +150,35 @@ IM2WIN_DEVICE void bulk_wait_read() {
 }
 IM2WIN_DEVICE void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
+IM2WIN_DEVICE int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+IM2WIN_DEVICE int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+
 struct ChunkGeom {
   uint32_t g0, nrows;
   uint64_t r_lo, f_begin, f_end, a_begin, a_end;
 };
+
+// Real input rows [lo, hi) that output row g reads (padded rows outside [0, H) are zeros).
+IM2WIN_DEVICE uint64_t in_row_lo(const TransformArgs& a, uint32_t g) {
+  uint32_t plane, m;
+  a.fd_ho.divmod(g, plane, m);
+  const int64_t r = static_cast<int64_t>(m) * a.stride - a.pad;
+  return static_cast<uint64_t>(plane) * a.h_in + static_cast<uint64_t>(imin64(imax64(r, 0), a.h_in));
+}
+IM2WIN_DEVICE uint64_t in_row_hi(const TransformArgs& a, uint32_t g) {
+  uint32_t plane, m;
+  a.fd_ho.divmod(g, plane, m);
+  const int64_t r = static_cast<int64_t>(m) * a.stride - a.pad + a.h_f;
+  return static_cast<uint64_t>(plane) * a.h_in + static_cast<uint64_t>(imin64(imax64(r, 0), a.h_in));
+}
 
 IM2WIN_DEVICE ChunkGeom chunk_geom(const PipeArgs& p, uint32_t chunk) {
   const TransformArgs& a = p.t;
   ChunkGeom c;
   c.g0 = chunk * a.rows_per_cta;
   c.nrows = min(a.rows_per_cta, a.rows_total - c.g0);
-  c.r_lo = in_row_of(a, c.g0);
-  const uint64_t r_hi = in_row_of(a, c.g0 + c.nrows - 1) + a.h_f;
+  c.r_lo = in_row_lo(a, c.g0);
+  const uint64_t r_hi = in_row_hi(a, c.g0 + c.nrows - 1);
   c.f_begin = c.r_lo * a.w_in;
   c.f_end = r_hi * a.w_in;
   c.a_begin = c.f_begin & ~3ull;
@@ -171,16 +189,38 @@ IM2WIN_DEVICE ChunkGeom chunk_geom(const PipeArgs& p, uint32_t chunk) {
 // Build one output chunk in shared memory.  Items (row gl, column col) are
 // strided by the CTA size; (gl, col) advances incrementally (no division in
 // the loop).  HF > 0 unrolls the Hf copies (loads first, then stores).
-template <int HF>
+// PAD: ro[gl] is the staged offset of padded row m*s - p, column -p (may point before
+// the tile); uv[gl] packs the valid tap range [u_lo, u_hi) of that output row.  A value
+// is read only when its row tap and column are inside the real input, else it is +0.
+template <int HF, bool PAD>
 IM2WIN_DEVICE void build_chunk(const TransformArgs& a, const float* __restrict__ tb, const int* __restrict__ ro,
-                               float* __restrict__ ob, uint32_t nrows, uint32_t tid, uint32_t dg, uint32_t dc) {
+                               const uint32_t* __restrict__ uv, float* __restrict__ ob, uint32_t nrows, uint32_t tid,
+                               uint32_t dg, uint32_t dc) {
   const uint32_t w_eff = a.w_eff, w_in = a.w_in, row_len = a.row_len;
   const uint32_t items = nrows * w_eff;
   uint32_t gl, col;
   a.fd_weff.divmod(tid, gl, col);
   for (uint32_t it = tid; it < items; it += kXformThreads) {
-    const float* tp = tb + ro[gl] + col;
-    if constexpr (HF > 0) {
+    const float* tp = tb + ro[gl] + static_cast<int>(col);
+    if constexpr (PAD) {
+      const uint32_t u_lo = uv[gl] & 0xffffu, u_hi = uv[gl] >> 16;
+      const bool col_ok = col >= a.pad && col < a.pad + w_in;
+      if constexpr (HF > 0) {
+        float* op = ob + gl * row_len + col * HF;
+        float v[HF];
+#pragma unroll
+        for (int u = 0; u < HF; ++u)
+          v[u] = (col_ok && static_cast<uint32_t>(u) >= u_lo && static_cast<uint32_t>(u) < u_hi)
+                     ? tp[static_cast<int>(u * w_in)] : 0.0f;
+#pragma unroll
+        for (int u = 0; u < HF; ++u) op[u] = v[u];
+      } else {
+        const uint32_t hf = a.h_f;
+        float* op = ob + gl * row_len + col * hf;
+        for (uint32_t u = 0; u < hf; ++u)
+          op[u] = (col_ok && u >= u_lo && u < u_hi) ? tp[static_cast<int>(u * w_in)] : 0.0f;
+      }
+    } else if constexpr (HF > 0) {
       float* op = ob + gl * row_len + col * HF;
       float v[HF];
 #pragma unroll
@@ -201,15 +241,16 @@ IM2WIN_DEVICE void build_chunk(const TransformArgs& a, const float* __restrict__
   }
 }
 
-template <int HF>
+template <int HF, bool PAD>
 __global__ void __launch_bounds__(kXformThreads) im2win_transform_pipe_kernel(const PipeArgs p) {
   const TransformArgs& a = p.t;
   uint32_t dg, dc;  // kXformThreads = dg * w_eff + dc
   a.fd_weff.divmod(kXformThreads, dg, dc);
   extern __shared__ __align__(16) float smem[];
   __shared__ __align__(8) uint64_t full[2];
-  int* rowoff = reinterpret_cast<int*>(smem);          // [2][rowoff_ints]
-  float* tile = smem + 2 * p.rowoff_ints;               // [2][tile_floats]
+  int* rowoff = reinterpret_cast<int*>(smem);          // [2][rowoff_ints] (+ [2][rowoff_ints] tap ranges if PAD)
+  uint32_t* urange = reinterpret_cast<uint32_t*>(rowoff + 2 * p.rowoff_ints);
+  float* tile = smem + (PAD ? 4 : 2) * p.rowoff_ints;  // [2][tile_floats]
   float* obuf = tile + 2 * a.tile_floats;               // [2][obuf_floats]
   const uint32_t tid = threadIdx.x;
 
@@ -240,9 +281,21 @@ __global__ void __launch_bounds__(kXformThreads) im2win_transform_pipe_kernel(co
     float* tb = tile + b * a.tile_floats;
     float* ob = obuf + b * p.obuf_floats;
     int* ro = rowoff + b * p.rowoff_ints;
+    uint32_t* uv = urange + b * p.rowoff_ints;
     const uint32_t tshift = static_cast<uint32_t>(c.f_begin - c.a_begin);
-    for (uint32_t gl = tid; gl < c.nrows; gl += blockDim.x)
-      ro[gl] = static_cast<int>((in_row_of(a, c.g0 + gl) - c.r_lo) * a.w_in + tshift);
+    for (uint32_t gl = tid; gl < c.nrows; gl += blockDim.x) {
+      if constexpr (PAD) {
+        uint32_t plane, m;
+        a.fd_ho.divmod(c.g0 + gl, plane, m);
+        const int64_t top = static_cast<int64_t>(m) * a.stride - a.pad;  // real row of tap u = 0
+        const int64_t row0 = static_cast<int64_t>(plane) * a.h_in + top - static_cast<int64_t>(c.r_lo);
+        ro[gl] = static_cast<int>(row0 * a.w_in - a.pad + tshift);
+        const int64_t u_lo = imax64(0, -top), u_hi = imin64(a.h_f, static_cast<int64_t>(a.h_in) - top);
+        uv[gl] = static_cast<uint32_t>(u_lo) | (static_cast<uint32_t>(imax64(u_hi, u_lo)) << 16);
+      } else {
+        ro[gl] = static_cast<int>((in_row_of(a, c.g0 + gl) - c.r_lo) * a.w_in + tshift);
+      }
+    }
 
     mbarrier_wait_parity(&full[b], (j >> 1) & 1);
     // input tail the bulk copy could not cover (end of the tensor, < 4 floats)
@@ -257,7 +310,7 @@ __global__ void __launch_bounds__(kXformThreads) im2win_transform_pipe_kernel(co
     const uint32_t count = c.nrows * a.row_len;
     const uint32_t head = min(count, static_cast<uint32_t>((4u - (e_begin & 3u)) & 3u));
     const uint32_t oshift = (4u - head) & 3u;
-    build_chunk<HF>(a, tb, ro, ob + oshift, c.nrows, tid, dg, dc);
+    build_chunk<HF, PAD>(a, tb, ro, uv, ob + oshift, c.nrows, tid, dg, dc);
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
 
@@ -283,24 +336,31 @@ struct TransformPlan {
   uint32_t grid;
 };
 
-static uint64_t host_in_row(uint64_t g, uint64_t h_out, uint64_t h_in, uint64_t s) {
-  return (g / h_out) * h_in + (g % h_out) * s;
+
+// Real input rows [lo, hi) of output row g with zero padding `pad` (pad = 0: hi = lo + h_f).
+static uint64_t host_row_lo(uint64_t g, uint64_t h_out, uint64_t h_in, uint64_t s, uint64_t pad) {
+  const int64_t r = static_cast<int64_t>((g % h_out) * s) - static_cast<int64_t>(pad);
+  return (g / h_out) * h_in + static_cast<uint64_t>(std::min<int64_t>(std::max<int64_t>(r, 0), h_in));
+}
+static uint64_t host_row_hi(uint64_t g, uint64_t h_out, uint64_t h_in, uint64_t s, uint64_t h_f, uint64_t pad) {
+  const int64_t r = static_cast<int64_t>((g % h_out) * s + h_f) - static_cast<int64_t>(pad);
+  return (g / h_out) * h_in + static_cast<uint64_t>(std::min<int64_t>(std::max<int64_t>(r, 0), h_in));
 }
 
-static uint32_t host_span(uint32_t R, uint32_t h_out, uint32_t h_in, uint32_t s, uint32_t h_f) {
+static uint32_t host_span(uint32_t R, uint32_t h_out, uint32_t h_in, uint32_t s, uint32_t h_f, uint32_t pad = 0) {
   // span of input rows read by output rows [p, p+R) maximised over the phase p.
   uint64_t best = 0;
   for (uint32_t p = 0; p < h_out; ++p) {
-    uint64_t lo = host_in_row(p, h_out, h_in, s);
-    uint64_t hi = host_in_row(p + R - 1, h_out, h_in, s) + h_f;
-    if (hi - lo > best) best = hi - lo;
+    uint64_t lo = host_row_lo(p, h_out, h_in, s, pad);
+    uint64_t hi = host_row_hi(p + R - 1, h_out, h_in, s, h_f, pad);
+    if (hi > lo && hi - lo > best) best = hi - lo;
   }
   return static_cast<uint32_t>(best);
 }
 
 static TransformPlan plan_transform(uint32_t rows_total, uint32_t h_out, uint32_t h_in, uint32_t w_in,
                                     uint32_t s, uint32_t h_f, uint32_t row_len, size_t smem_cap,
-                                    uint32_t target_floats = 8192) {
+                                    uint32_t target_floats = 8192, uint32_t pad = 0) {
   TransformPlan p{};
   uint32_t R = (target_floats + row_len - 1) / row_len;
   uint32_t min_r = (2 * h_f + s - 1) / s;
@@ -308,7 +368,7 @@ static TransformPlan plan_transform(uint32_t rows_total, uint32_t h_out, uint32_
   if (R > rows_total) R = rows_total;
   if (R < 1) R = 1;
   for (;;) {
-    p.span = host_span(R, h_out, h_in, s, h_f);
+    p.span = host_span(R, h_out, h_in, s, h_f, pad);
     p.tile_floats = (p.span * w_in + 3 + 3) & ~3u;
     const size_t out_floats = static_cast<size_t>(R) * row_len + 3;
     p.smem_bytes = (static_cast<size_t>((R + 3) & ~3u) + p.tile_floats + out_floats) * 4;
@@ -324,7 +384,7 @@ static TransformPlan plan_transform(uint32_t rows_total, uint32_t h_out, uint32_
 
 // Launcher used by the C ABI (capi.cu).
 int im2win_launch_transform(const float* src, float* dst, int64_t n, int64_t c, int64_t h, int64_t w,
-                            int h_f, int w_f, int stride, int64_t h_out, int64_t w_eff,
+                            int h_f, int w_f, int stride, int64_t h_out, int64_t w_eff, int pad,
                             cudaStream_t stream, const char** err) {
   using namespace im2win;
   const int64_t rows_total = n * c * h_out;
@@ -358,6 +418,7 @@ int im2win_launch_transform(const float* src, float* dst, int64_t n, int64_t c, 
   a.fd_rl = FastDiv(a.row_len);
   a.fd_hf = FastDiv(a.h_f);
   a.fd_weff = FastDiv(a.w_eff);
+  a.pad = static_cast<uint32_t>(pad);
   (void)w_f;
   const bool aligned = (reinterpret_cast<uintptr_t>(src) & 15u) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
   // pipelined path: two stages of (row offsets, staged input, output chunk)
@@ -365,7 +426,8 @@ int im2win_launch_transform(const float* src, float* dst, int64_t n, int64_t c, 
   const uint32_t target = tgt_env ? static_cast<uint32_t>(atoi(tgt_env)) : 4096u;
   TransformPlan q = plan_transform(static_cast<uint32_t>(rows_total), static_cast<uint32_t>(h_out),
                                    static_cast<uint32_t>(h), static_cast<uint32_t>(w), static_cast<uint32_t>(stride),
-                                   static_cast<uint32_t>(h_f), static_cast<uint32_t>(row_len), 48 * 1024, target);
+                                   static_cast<uint32_t>(h_f), static_cast<uint32_t>(row_len), 48 * 1024, target,
+                                   static_cast<uint32_t>(pad));
   PipeArgs pa;
   pa.t = a;
   pa.t.rows_per_cta = q.rows_per_cta;
@@ -374,17 +436,22 @@ int im2win_launch_transform(const float* src, float* dst, int64_t n, int64_t c, 
   pa.rowoff_ints = (q.rows_per_cta + 3) & ~3u;
   pa.src_floats = static_cast<uint64_t>(n * c * h * w);
   pa.n_chunks = q.grid;
-  const size_t pipe_smem = 2ull * (pa.rowoff_ints + pa.t.tile_floats + pa.obuf_floats) * 4;
+  const size_t pipe_smem = 2ull * ((pad ? 2 : 1) * pa.rowoff_ints + pa.t.tile_floats + pa.obuf_floats) * 4;
+  if (pad && !(aligned && pipe_smem <= 200 * 1024)) {
+    *err = "im2win_transform_f32: zero padding needs 16-byte aligned buffers";
+    return 1;
+  }
   if (aligned && pipe_smem <= 200 * 1024) {
-    void (*kern)(const PipeArgs) = im2win_transform_pipe_kernel<0>;
+    void (*kern)(const PipeArgs) = im2win_transform_pipe_kernel<0, false>;
     int ki = 0;
     switch (h_f) {
-      case 3: kern = im2win_transform_pipe_kernel<3>; ki = 1; break;
-      case 5: kern = im2win_transform_pipe_kernel<5>; ki = 2; break;
-      case 7: kern = im2win_transform_pipe_kernel<7>; ki = 3; break;
-      case 11: kern = im2win_transform_pipe_kernel<11>; ki = 4; break;
-      default: break;
+      case 3: kern = pad ? im2win_transform_pipe_kernel<3, true> : im2win_transform_pipe_kernel<3, false>; ki = 1; break;
+      case 5: kern = pad ? im2win_transform_pipe_kernel<5, true> : im2win_transform_pipe_kernel<5, false>; ki = 2; break;
+      case 7: kern = pad ? im2win_transform_pipe_kernel<7, true> : im2win_transform_pipe_kernel<7, false>; ki = 3; break;
+      case 11: kern = pad ? im2win_transform_pipe_kernel<11, true> : im2win_transform_pipe_kernel<11, false>; ki = 4; break;
+      default: kern = pad ? im2win_transform_pipe_kernel<0, true> : im2win_transform_pipe_kernel<0, false>; break;
     }
+    ki += pad ? 8 : 0;
     // per-(kernel, smem size) occupancy cache: keeps host work per call small
     static thread_local struct { int dev, ki; size_t smem; int occ; int sms; } cache[8];
     static thread_local int cache_n = 0;

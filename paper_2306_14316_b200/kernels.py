@@ -163,13 +163,16 @@ def conv_cl_into(win_cl: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, par
     _lib.check(rc)
 
 
-def nhwc_into(src: torch.Tensor, dst: torch.Tensor) -> None:
-    """NCHW float32 -> channels-last copy (float32 or bfloat16) for the fused TC path."""
+def nhwc_into(src: torch.Tensor, dst: torch.Tensor, pad: int = 0) -> None:
+    """NCHW float32 -> channels-last copy (float32 or bfloat16) for the fused TC path.
+
+    pad > 0: dst is (N, H + 2*pad, W + 2*pad, pitch) and its border pixels are zeroed.
+    """
     n_img, c_in, h_in, w_in = (int(d) for d in src.shape)
     dtype = 1 if dst.dtype == torch.bfloat16 else 0
     with torch.cuda.device(src.device):
-        rc = _lib.load().im2win_nchw_to_nhwc(src.data_ptr(), dst.data_ptr(), n_img, c_in, h_in, w_in, dtype,
-                                             torch.cuda.current_stream(src.device).cuda_stream)
+        rc = _lib.load().im2win_nchw_to_nhwc_padded(src.data_ptr(), dst.data_ptr(), n_img, c_in, h_in, w_in, dtype,
+                                                    pad, torch.cuda.current_stream(src.device).cuda_stream)
     _lib.check(rc)
 
 
@@ -221,12 +224,16 @@ def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, 
     if variant in ("tf32", "bf16") and tc_path in ("auto", "fused"):
         dt = torch.bfloat16 if variant == "bf16" else torch.float32
         n_img, c_in, h_in, w_in = i.dims
-        x_cl = torch.empty((n_img, h_in, w_in, nhwc_pitch(c_in, variant)), dtype=dt, device=i.device)
-        nhwc_into(i.data, x_cl)
+        pad = params.pad
+        x_cl = torch.empty((n_img, h_in + 2 * pad, w_in + 2 * pad, nhwc_pitch(c_in, variant)), dtype=dt,
+                           device=i.device)
+        nhwc_into(i.data, x_cl, pad)
         out = torch.empty((n_img, params.c_out, h_out, w_out), dtype=DTYPE, device=i.device)
         fd = f.data if f.device == i.device else f.data.to(i.device)
         conv_fused_into(x_cl, fd, out, params, variant)
         return Tensor4(out)
+    if ok and tc_path == "cl" and params.pad:
+        raise ValueError("tc_path='cl' has no zero padding; use 'fused' or 'gather'")
     if ok and tc_path == "cl":
         dt = torch.bfloat16 if variant == "bf16" else torch.float32
         win_cl = torch.empty(im2win_cl_shape(i.dims, params), dtype=dt, device=i.device)
@@ -313,12 +320,12 @@ def conv_im2win_opt_host(inp, flt, params: ConvParams, plan: TilePlan | None = N
     code = _variant_code(variant)
     lib = _lib.load()
     nbytes = lib.im2win_conv_host_workspace_bytes(n_img, c_in, h_in, w_in, params.c_out, params.h_f, params.w_f,
-                                                  params.stride, code, chunk_images)
+                                                  params.stride, params.pad, code, chunk_images)
     stream = torch.cuda.current_stream(dev).cuda_stream
     cplan = to_c_plan(plan)
     cp = None if cplan is None else _byref(cplan)
     args = (x.data_ptr(), f.data_ptr(), out.data_ptr(), n_img, c_in, h_in, w_in, params.c_out, params.h_f,
-            params.w_f, params.stride, cp, code, chunk_images)
+            params.w_f, params.stride, params.pad, cp, code, chunk_images)
     if wait:
         ws = _workspace(dev, stream, nbytes)
         _lib.check(lib.im2win_conv_host_f32(*args, ws.data_ptr(), ws.numel(), stream))

@@ -85,19 +85,27 @@ class Tensor4:
 
 @dataclass(frozen=True)
 class ConvParams:
-    """Filter geometry plus a single stride applied to both spatial axes (tensors.py:94-112)."""
+    """Filter geometry plus a single stride applied to both spatial axes (tensors.py:94-112).
+
+    `pad` (extension, default 0 = the reference's unpadded convolution) zero-pads the
+    input by `pad` on every side inside the transform; the padded input is never
+    materialised and the result is bit-identical to convolving an explicitly padded input.
+    """
 
     c_in: int
     c_out: int
     h_f: int
     w_f: int
     stride: int = 1
+    pad: int = 0
 
     def __post_init__(self):
         for name in ("c_in", "c_out", "h_f", "w_f", "stride"):
             value = getattr(self, name)
             if int(value) != value or value < 1:
                 raise GeometryError(f"{name} must be a positive integer, got {value}")
+        if int(self.pad) != self.pad or self.pad < 0:
+            raise GeometryError(f"pad must be a non-negative integer, got {self.pad}")
 
     @property
     def filter_dims(self) -> tuple[int, int, int, int]:
@@ -105,7 +113,8 @@ class ConvParams:
 
 
 def output_dims(h_in: int, w_in: int, params: ConvParams) -> tuple[int, int]:
-    """Unpadded output extents: floor((in - filter) / stride) + 1 per axis (tensors.py:115-123)."""
+    """Output extents: floor((in + 2*pad - filter) / stride) + 1 per axis (tensors.py:115-123, pad = 0)."""
+    h_in, w_in = h_in + 2 * params.pad, w_in + 2 * params.pad
     if params.h_f > h_in or params.w_f > w_in:
         raise GeometryError(
             f"filter {params.h_f}x{params.w_f} larger than input {h_in}x{w_in}"

@@ -375,3 +375,60 @@ def test_nhwc_copy_exact(shape, dtype):
     ref[..., :c] = x.permute(0, 2, 3, 1).to(dtype)
     assert torch.equal(out.view(torch.int16 if dtype == torch.bfloat16 else torch.int32),
                        ref.view(torch.int16 if dtype == torch.bfloat16 else torch.int32))
+
+
+def _pad_np(x, p):
+    return np.pad(x, ((0, 0), (0, 0), (p, p), (p, p)))
+
+
+def test_native_padding_config1_golden(layer_goldens):
+    """Config 1 (pad 1) with the padding done inside the transform gives the reference's
+    bits for the explicitly pre-padded input (golden checksum cfg1-pad1)."""
+    padded, flt = make_config1_inputs(0)
+    inp = np.ascontiguousarray(padded[:, :, 1:57, 1:57])
+    params = pkg.ConvParams(64, 64, 3, 3, 1, pad=1)
+    out = pkg.conv_im2win_opt(inp, flt, params)
+    assert orc.checksum(out.numpy()) == layer_goldens["cfg1-pad1"]["out_sha"]
+    host = pkg.conv_im2win_opt_host(inp, flt, params)
+    assert orc.checksum(host.numpy()) == layer_goldens["cfg1-pad1"]["out_sha"]
+
+
+@pytest.mark.parametrize("case", [(2, 3, 9, 11, 4, 3, 3, 1, 1), (1, 5, 7, 6, 3, 3, 2, 2, 2), (3, 2, 5, 5, 2, 2, 2, 1, 3),
+                                  (1, 4, 12, 13, 5, 7, 7, 2, 3), (2, 3, 6, 8, 2, 11, 11, 4, 5),
+                                  (1, 64, 56, 56, 8, 3, 3, 1, 1), (1, 16, 20, 17, 4, 5, 5, 2, 4)])
+def test_native_padding_transform_and_conv(case):
+    """Padded transform == transform of the explicitly padded input (bitwise, incl. pad >= Hf:
+    all-zero window rows); fp32-exact conv == the oracle on the padded input (bitwise)."""
+    n, c, h, w, co, hf, wf, s, p = case
+    rng = np.random.default_rng(sum(case))
+    inp = rng.standard_normal((n, c, h, w), dtype=np.float32)
+    flt = rng.standard_normal((co, c, hf, wf), dtype=np.float32)
+    params = pkg.ConvParams(c, co, hf, wf, s, pad=p)
+    win = pkg.im2win(inp, params)
+    ref_win = orc.im2win_fill(_pad_np(inp, p), hf, wf, s)
+    assert bits_equal(win.data.cpu().numpy(), ref_win), case
+    out = pkg.conv_im2win_opt(inp, flt, params)
+    assert bits_equal_nan_as_class(out.numpy(), orc.conv_direct(_pad_np(inp, p), flt, s)), case
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_native_padding_tensor_cores(variant):
+    """TC variants with padding: the channels-last copy writes zero borders, every fused kernel
+    and the gather path stay within tolerance; the host pipeline matches the device path."""
+    cases = [(2, 64, 28, 28, 64, 3, 3, 1, 1), (1, 64, 30, 30, 64, 7, 7, 2, 3), (2, 3, 32, 32, 64, 3, 3, 1, 1),
+             (1, 96, 12, 12, 128, 5, 5, 1, 2)]
+    for (n, c, h, w, co, hf, wf, s, p) in cases:
+        rng = np.random.default_rng(h * 7 + p)
+        inp = rng.standard_normal((n, c, h, w), dtype=np.float32)
+        flt = rng.standard_normal((co, c, hf, wf), dtype=np.float32)
+        params = pkg.ConvParams(c, co, hf, wf, s, pad=p)
+        ref = orc.conv_direct(_pad_np(inp, p), flt, s)
+        for path in ("fused", "gather"):
+            out = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path=path).numpy()
+            assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (n, c, h, w, p, path)
+        dev = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path="fused").numpy()
+        host = pkg.conv_im2win_opt_host(inp, flt, params, variant=variant, chunk_images=1).numpy()
+        assert bits_equal(host, dev)
+    with pytest.raises(ValueError):
+        pkg.conv_im2win_opt(np.zeros((1, 8, 8, 8), np.float32), np.zeros((8, 8, 3, 3), np.float32),
+                            pkg.ConvParams(8, 8, 3, 3, 1, pad=1), variant=variant, tc_path="cl")

@@ -141,3 +141,15 @@ def test_tile_pick_mirrors_library():
     for m in (1, 32, 64, 96, 100, 192, 512):
         for n in (1, 1000, 10 ** 5, 3 * 10 ** 6):
             assert simt_tile_for(pkg.GemmDims(m, n, 9)) == lib.im2win_simt_pick(m, n, 9), (m, n)
+
+
+def test_output_dims_with_padding():
+    p = pkg.ConvParams(64, 64, 3, 3, 1, pad=1)
+    assert pkg.output_dims(56, 56, p) == (56, 56)
+    assert pkg.output_dims(224, 224, pkg.ConvParams(3, 64, 7, 7, 2, pad=3)) == (112, 112)
+    assert pkg.output_dims(2, 2, pkg.ConvParams(1, 1, 3, 3, 1, pad=1)) == (2, 2)
+    with pytest.raises(pkg.GeometryError):
+        pkg.ConvParams(1, 1, 3, 3, 1, pad=-1)
+    with pytest.raises(pkg.GeometryError):
+        pkg.output_dims(1, 1, pkg.ConvParams(1, 1, 5, 5, 1, pad=1))
+    assert pkg.ConvParams(1, 1, 3, 3) == pkg.ConvParams(1, 1, 3, 3, 1, 0)

@@ -6,7 +6,7 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import torch  # noqa: E402
 
-from paper_2306_14316_b200.kernels import conv_fused_into, nhwc_into  # noqa: E402
+from paper_2306_14316_b200.kernels import conv_fused_into, nhwc_into, nhwc_pitch  # noqa: E402
 from paper_2306_14316_b200.workloads import BENCHMARKS  # noqa: E402
 
 name, variant = sys.argv[1], sys.argv[2]
@@ -17,7 +17,7 @@ dev = torch.device("cuda:0")
 h_out, w_out = cfg.out_dims
 x = torch.randn((cfg.batch, cfg.c_in, cfg.h_in, cfg.w_in), device=dev)
 f = torch.randn((cfg.c_out, cfg.c_in, cfg.h_f, cfg.w_f), device=dev)
-xc = torch.empty((cfg.batch, cfg.h_in, cfg.w_in, cfg.c_in), device=dev,
+xc = torch.empty((cfg.batch, cfg.h_in, cfg.w_in, nhwc_pitch(cfg.c_in, variant)), device=dev,
                  dtype=torch.bfloat16 if variant == "bf16" else torch.float32)
 o = torch.empty((cfg.batch, cfg.c_out, h_out, w_out), device=dev)
 for _ in range(reps):
