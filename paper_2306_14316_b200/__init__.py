@@ -27,6 +27,7 @@ from .kernels import (
     conv_im2win_basic,
     conv_im2win_opt,
     conv_im2win_opt_host,
+    conv_im2win_opt_host_batch,
 )
 from .workloads import BENCHMARKS, BenchConfig, make_inputs
 from .fixture_io import read_tensor, write_tensor
@@ -59,6 +60,7 @@ __all__ = [
     "conv_im2win_basic",
     "conv_im2win_opt",
     "conv_im2win_opt_host",
+    "conv_im2win_opt_host_batch",
     "decompose_k",
     "decompose_n",
     "default_plan",

@@ -33,7 +33,7 @@ int im2win_set_error(int code, const char* msg);
 namespace {
 
 constexpr int kMaxDev = 64;
-constexpr int kMaxDepth = 4;  // input / output chunk buffers in flight (runtime depth <= this)
+constexpr int kMaxDepth = 8;  // input / output chunk buffers in flight (runtime depth <= this)
 constexpr int kRing = 256;  // completion events of non-blocking submissions
 
 struct DevPipe {
@@ -89,18 +89,21 @@ Geometry geometry(int64_t n_chunk, int64_t c_in, int64_t h, int64_t w, int64_t c
   return g;
 }
 
-int depth() {
-  static int d = [] {
+// Chunk buffers per call: one per chunk up to kMaxDepth, so a call's compute never waits
+// for its own downloads (measured: with 2 buffers, compute of a download-heavy layer is
+// paced by PCIe and stalls every later call on the compute stream).  IM2WIN_HOST_DEPTH caps it.
+int depth_for(int64_t n_chunks) {
+  static int cap = [] {
     const char* e = getenv("IM2WIN_HOST_DEPTH");
-    int v = e ? atoi(e) : 2;
-    return v < 2 ? 2 : (v > kMaxDepth ? kMaxDepth : v);
+    int v = e ? atoi(e) : kMaxDepth;
+    return v < 1 ? 1 : (v > kMaxDepth ? kMaxDepth : v);
   }();
-  return d;
+  return static_cast<int>(std::min<int64_t>(n_chunks, cap));
 }
 
-size_t workspace_bytes(const Geometry& g) {
+size_t workspace_bytes(const Geometry& g, int64_t n_chunks) {
   return align_up(g.flt_elems * 4) + align_up(g.conv_ws) + align_up(g.mid_bytes) +
-         depth() * (align_up(g.in_elems * 4) + align_up(g.out_elems * 4));
+         depth_for(n_chunks) * (align_up(g.in_elems * 4) + align_up(g.out_elems * 4));
 }
 
 int64_t pick_chunk(int64_t n, int64_t chunk) {
@@ -121,7 +124,7 @@ size_t im2win_conv_host_workspace_bytes(int64_t n, int64_t c_in, int64_t h, int6
       h_f > h + 2 * pad || w_f > w + 2 * pad)
     return 0;
   const int64_t cn = pick_chunk(n, chunk_images);
-  return workspace_bytes(geometry(cn, c_in, h, w, c_out, h_f, w_f, stride, pad, variant));
+  return workspace_bytes(geometry(cn, c_in, h, w, c_out, h_f, w_f, stride, pad, variant), (n + cn - 1) / cn);
 }
 
 }  // extern "C"
@@ -139,7 +142,8 @@ static int host_conv(const float* host_in, const float* host_flt, float* host_ou
     return im2win_set_error(1, "im2win_conv_host_f32: unknown variant");
   const int64_t cn = pick_chunk(n, chunk_images);
   const Geometry g = geometry(cn, c_in, h, w, c_out, h_f, w_f, stride, pad, variant);
-  if (ws_bytes < workspace_bytes(g)) return im2win_set_error(1, "im2win_conv_host_f32: workspace too small");
+  const int64_t n_chunks = (n + cn - 1) / cn;
+  if (ws_bytes < workspace_bytes(g, n_chunks)) return im2win_set_error(1, "im2win_conv_host_f32: workspace too small");
 
   cudaPointerAttributes attr;
   if (cudaPointerGetAttributes(&attr, workspace) != cudaSuccess || attr.type != cudaMemoryTypeDevice)
@@ -173,7 +177,7 @@ static int host_conv(const float* host_in, const float* host_flt, float* host_ou
   base += align_up(g.conv_ws);
   void* mid = base;
   base += align_up(g.mid_bytes);
-  const int D = depth();
+  const int D = depth_for(n_chunks);
   float* d_in[kMaxDepth];
   float* d_out[kMaxDepth];
   for (int i = 0; i < D; ++i) {
@@ -193,7 +197,6 @@ static int host_conv(const float* host_in, const float* host_flt, float* host_ou
 
   const int64_t img_in = c_in * h * w;
   const int64_t img_out = c_out * g.h_out * g.w_out;
-  const int64_t n_chunks = (n + cn - 1) / cn;
   int rc = 0;
   for (int64_t k = 0; k < n_chunks && rc == 0; ++k) {
     const int s = static_cast<int>(k % D);

@@ -336,3 +336,31 @@ def conv_im2win_opt_host(inp, flt, params: ConvParams, plan: TilePlan | None = N
     ticket = ctypes.c_int64(-1)
     _lib.check(lib.im2win_conv_host_submit(*args, ws.data_ptr(), ws.numel(), stream, ctypes.byref(ticket)))
     return HostConv(out, ticket.value, (x, f, ws, cplan))
+
+
+def conv_im2win_opt_host_batch(jobs, *, variant: str = "fp32-exact", outs=None, chunk_images: int = 0,
+                               device=None) -> list:
+    """Several independent host-operand convolutions (e.g. the layers of a benchmark step).
+
+    `jobs` is a list of (inp, flt, params); `outs` optional page-locked outputs in the same
+    order.  All jobs are submitted non-blocking to the streamed host pipeline, ordered so
+    the PCIe download engine starts early: jobs that download more than they upload go
+    first, upload-heavy jobs last (uploads of one job overlap downloads of the ones before
+    it).  Returns the host outputs in the order of `jobs`.
+    """
+    def elems(x):
+        return int(np.prod(x.shape)) if hasattr(x, "shape") else int(np.prod(x.data.shape))
+
+    balance = []
+    for inp, flt, params in jobs:
+        shape = inp.shape if hasattr(inp, "shape") else inp.data.shape
+        h_out, w_out = output_dims(int(shape[2]), int(shape[3]), params)
+        d2h = int(shape[0]) * params.c_out * h_out * w_out
+        balance.append(d2h - elems(inp))
+    order = sorted(range(len(jobs)), key=lambda i: -balance[i])
+    handles = [None] * len(jobs)
+    for i in order:
+        inp, flt, params = jobs[i]
+        handles[i] = conv_im2win_opt_host(inp, flt, params, variant=variant, chunk_images=chunk_images,
+                                          out=None if outs is None else outs[i], device=device, wait=False)
+    return [h.wait() for h in handles]

@@ -432,3 +432,15 @@ def test_native_padding_tensor_cores(variant):
     with pytest.raises(ValueError):
         pkg.conv_im2win_opt(np.zeros((1, 8, 8, 8), np.float32), np.zeros((8, 8, 3, 3), np.float32),
                             pkg.ConvParams(8, 8, 3, 3, 1, pad=1), variant=variant, tc_path="cl")
+
+
+def test_host_batch_api_order_and_bits():
+    """The batch host API returns results in job order, bit-identical to one-by-one calls."""
+    jobs = []
+    for i, name in enumerate(["conv7", "conv12", "conv4", "conv9"]):
+        cfg = replace(BENCHMARKS[name], batch=2 + i % 2, seed=60 + i)
+        inp, flt = make_inputs(cfg)
+        jobs.append((inp, flt, cfg.params))
+    outs = pkg.conv_im2win_opt_host_batch(jobs)
+    for (inp, flt, params), out in zip(jobs, outs):
+        assert bits_equal(out.numpy(), pkg.conv_im2win_opt(inp, flt, params).numpy())
