@@ -392,8 +392,11 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
   a.vec_out = (hw % 4 == 0) ? 1u : 0u;
 
   cudaError_t e = cudaSuccess;
+#ifndef IM2WIN_SIMT_STAGES
+#define IM2WIN_SIMT_STAGES 3
+#endif
 #define IM2WIN_DISPATCH(BM_, BN_, BK_)                                                              \
-  if (exact && vec && stages == 3) e = launch_cfg<BM_, BN_, BK_, 3, true, true, 8>(a, stream);       \
+  if (exact && vec && stages == 3) e = launch_cfg<BM_, BN_, BK_, IM2WIN_SIMT_STAGES, true, true, 8>(a, stream); \
   else if (exact && vec && stages == 1) e = launch_cfg<BM_, BN_, BK_, 1, true, true, 8>(a, stream);  \
   else if (exact && !vec) e = launch_cfg<BM_, BN_, BK_, 3, true, false, 8>(a, stream);               \
   else if (!exact && vec) e = launch_cfg<BM_, BN_, BK_, 3, false, true, 8>(a, stream);               \
