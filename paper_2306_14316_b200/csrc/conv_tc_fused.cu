@@ -15,6 +15,7 @@
 // Hf*Wf/s^2 window overlap) -- versus writing and re-reading the 2-4x larger Ĩ.
 #include <stddef.h>
 #include <algorithm>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "tc_common.cuh"
@@ -185,12 +186,15 @@ struct FusedArgs {
   uint32_t k_slabs, fh_slabs;  // k_slabs = Hf * fh_slabs
 };
 
-template <bool BF16, int N, int STAGES>
+// RB: the whole packed filter (k_slabs tiles of N x 128 B) is loaded once per CTA and
+// stays resident; only window tiles stream through the ring (small filters: the
+// 3-channel input layers, where staging the filter per tile doubles the TMA rows).
+template <bool BF16, int N, int STAGES, bool RB = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
     conv_tc_fused_kernel(const FusedArgs a, const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b) {
   constexpr uint32_t kABytes = kTileM * kRowBytes;
-  constexpr uint32_t kBBytes = N * kRowBytes;
+  constexpr uint32_t kBBytes = RB ? 0 : N * kRowBytes;
   constexpr uint32_t kStageBytes = kABytes + kBBytes;
   constexpr int kBK = BF16 ? 64 : 32;
   constexpr int kUK = BF16 ? 16 : 8;
@@ -202,19 +206,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
   __shared__ __align__(8) uint64_t tfull_bar[2];
   __shared__ __align__(8) uint64_t tempty_bar[2];
+  __shared__ __align__(8) uint64_t bres_bar;
   __shared__ uint32_t tmem_base_sh;
 
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const uint32_t pix_per_tile = a.box_w * a.box_h * a.box_n;
   const uint32_t a_box_bytes = pix_per_tile * kRowBytes;
+  // RB: resident filter tiles first, then the A ring
+  const uint32_t rb_bytes = RB ? a.k_slabs * N * kRowBytes : 0;
+  uint8_t* smem = smem_base + rb_bytes;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
+    mbar_init(&bres_bar, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], kEpiWarps);
@@ -237,6 +246,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
+      if constexpr (RB) {  // requires co_tiles == 1 (host-checked)
+        mbar_arrive_expect_tx(&bres_bar, rb_bytes);
+        for (uint32_t ks = 0; ks < a.k_slabs; ++ks)
+          tma_load_2d(smem_base + ks * N * kRowBytes, &tmap_b, &bres_bar, ks * kBK, 0);
+      }
       for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         const uint32_t co_blk = t % a.co_tiles;
         uint32_t pt = t / a.co_tiles;
@@ -255,7 +269,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               "%7}], [%2];\n" ::"r"(smem_u32(st)),
               "l"(&tmap_a), "r"(smem_u32(&full_bar[stage])), "r"(j0), "r"(fh), "r"(ow0), "r"(oh0), "r"(n0)
               : "memory");
-          tma_load_2d(st + kABytes, &tmap_b, &full_bar[stage], ks * kBK, co_blk * N);
+          if constexpr (!RB) tma_load_2d(st + kABytes, &tmap_b, &full_bar[stage], ks * kBK, co_blk * N);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -263,6 +277,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      if constexpr (RB) mbar_wait(&bres_bar, 0);
       for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -271,7 +286,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t abase = smem_u32(smem + stage * kStageBytes);
-          const uint32_t bbase = abase + kABytes;
+          const uint32_t bbase = RB ? smem_u32(smem_base) + ks * N * kRowBytes : abase + kABytes;
 #pragma unroll
           for (int kk = 0; kk < kBK / kUK; ++kk)
             mma<BF16>(tmem_d, smem_desc_sw128(abase + kk * 32), smem_desc_sw128(bbase + kk * 32), kIdesc,
@@ -353,7 +368,7 @@ __global__ void pack_filter_fused_kernel(const float* __restrict__ flt, void* __
   }
 }
 
-template <bool BF16, int N, int STAGES>
+template <bool BF16, int N, int STAGES, bool RB = false>
 static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64_t c_in, int64_t h, int64_t w,
                         int32_t h_f, int32_t w_f, int32_t stride, int64_t Kp, int64_t Mp, cudaStream_t stream,
                         const char** err) {
@@ -394,8 +409,9 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
     }
   }
   a.co_tiles = static_cast<uint32_t>(Mp / N);
-  const size_t smem = static_cast<size_t>(STAGES) * (kTileM + N) * kRowBytes + 1024;
-  auto kern = conv_tc_fused_kernel<BF16, N, STAGES>;
+  const size_t rb = RB ? static_cast<size_t>(a.k_slabs) * N * kRowBytes : 0;
+  const size_t smem = rb + static_cast<size_t>(STAGES) * (kTileM + (RB ? 0 : N)) * kRowBytes + 1024;
+  auto kern = conv_tc_fused_kernel<BF16, N, STAGES, RB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
@@ -406,7 +422,10 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t tiles = static_cast<uint64_t>(a.n_tiles) * a.oh_tiles * a.ow_tiles * a.co_tiles;
   const uint32_t grid = tiles < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(tiles) : static_cast<uint32_t>(sms);
-  im2win_note_kernel(BF16 ? "conv_tc_fused_kernel (generic TMA window boxes, bf16)" : "conv_tc_fused_kernel (generic TMA window boxes, tf32)");
+  im2win_note_kernel(RB ? (BF16 ? "conv_tc_fused_kernel (generic TMA window boxes, filter resident, bf16)"
+                              : "conv_tc_fused_kernel (generic TMA window boxes, filter resident, tf32)")
+                     : (BF16 ? "conv_tc_fused_kernel (generic TMA window boxes, bf16)"
+                             : "conv_tc_fused_kernel (generic TMA window boxes, tf32)"));
   kern<<<grid, kTcThreads, smem, stream>>>(a, map_a, map_b);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -572,6 +591,31 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
                                                              static_cast<int>(Kp));
 #define IM2WIN_FU(BF, NN, ST) \
   return launch_fused<BF, NN, ST>(a, x_cl, workspace, cp, h, w, h_f, w_f, stride, Kp, Mp, stream, err)
+#define IM2WIN_FU_RB(BF, NN) \
+  return launch_fused<BF, NN, 6, true>(a, x_cl, workspace, cp, h, w, h_f, w_f, stride, Kp, Mp, stream, err)
+  {
+    // filter-resident mode: one Co tile whose whole packed filter fits beside 6 window stages
+    const char* rb_env = getenv("IM2WIN_FUSED_RB");
+    const size_t rb_bytes = static_cast<size_t>(a.k_slabs) * N * kRowBytes;
+    const bool rb = Mp == N && (N == 64 || N == 96 || N == 128) &&
+                    rb_bytes + 6 * kTileM * kRowBytes + 1024 <= 227 * 1024 && !(rb_env && atoi(rb_env) == 0);
+    if (rb) {
+      if (bf16) {
+        switch (N) {
+          case 64: IM2WIN_FU_RB(true, 64);
+          case 96: IM2WIN_FU_RB(true, 96);
+          default: IM2WIN_FU_RB(true, 128);
+        }
+      } else {
+        switch (N) {
+          case 64: IM2WIN_FU_RB(false, 64);
+          case 96: IM2WIN_FU_RB(false, 96);
+          default: IM2WIN_FU_RB(false, 128);
+        }
+      }
+    }
+  }
+#undef IM2WIN_FU_RB
   if (bf16) {
     switch (N) {
       case 64: IM2WIN_FU(true, 64, 8);
