@@ -44,6 +44,16 @@ def load_peaks() -> dict:
     return dict(PEAKS_FALLBACK)
 
 
+def max_rel_diff_device(a, b) -> float:
+    """winconv max_rel_diff (tensors.py:135-150) evaluated on the GPU: identical bits -> 0."""
+    import torch
+
+    a64, b64 = a.double(), b.double()
+    d = (a64 - b64).abs() / torch.clamp(torch.maximum(a64.abs(), b64.abs()), min=1.0)
+    d[a.view(torch.int32) == b.view(torch.int32)] = 0
+    return float(d.max().item())
+
+
 def set_fp32_precision(mode: str) -> None:
     """Float32 conv/matmul precision of the PyTorch baselines: "ieee" (true FP32) or "tf32".
 
@@ -352,6 +362,26 @@ def main() -> None:
                                 "im2win": 4 * cfg.elems("im2win")},
         })
 
+    # ---- the FFMA variant (within 1e-4 of the reference, not bit-exact), same step for context ----
+    fma = None
+    if args.variant == "fp32-exact" and rank == 0:
+        fma_out = [torch.empty_like(L["out"]) for L in layers]
+        for L, o in zip(layers, fma_out):  # warm-up
+            conv_windows_into(L["win"], L["f"], o, L["cfg"].params, L["cfg"].w_eff, None, "fp32-fma")
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(layers) + 1)]
+        ev[0].record(stream)
+        for i, (L, o) in enumerate(zip(layers, fma_out)):
+            im2win_into(L["x"], L["win"], L["cfg"].params)
+            conv_windows_into(L["win"], L["f"], o, L["cfg"].params, L["cfg"].w_eff, None, "fp32-fma")
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize(dev)
+        fma = {"step_tflops": flops_step / (ev[0].elapsed_time(ev[-1]) * 1e-3) / 1e12,
+               "max_rel_diff_vs_exact": max(max_rel_diff_device(o, L["out"]) for L, o in zip(layers, fma_out)),
+               "layers_tflops": {L["cfg"].name: L["cfg"].flops / (ev[i].elapsed_time(ev[i + 1]) * 1e-3) / 1e12
+                                 for i, L in enumerate(layers)},
+               "note": "transform + FFMA conv (ascending k, one rounding per multiply-add); bounded by the FFMA peak"}
+        del fma_out
+
     # ---- FP32 CUDA-core peak probe (roofline denominator) ----
     lib = _lib.load()
     sink = torch.empty(256, device=dev)
@@ -615,6 +645,7 @@ def main() -> None:
         "clocks": clocks,
         "layers": per_layer,
         "baselines": baselines,
+        "fp32_fma_variant": fma,
         "tensor_core_variants": tc,
         "peaks": {"fp32_exact_tflops": peak["exact"], "fp32_ffma_tflops": peak["ffma"],
                   "hbm_gbs": peaks["hbm_gbs"], "source": peaks["source"]},
