@@ -89,6 +89,29 @@ def _make_device_inputs(cfg: BenchConfig, device) -> tuple[torch.Tensor, torch.T
     return x, f
 
 
+class _IeeeFp32:
+    """True-FP32 PyTorch baselines: torch 2.11 runs cuDNN float32 convolutions in TF32 by default."""
+
+    def __enter__(self):
+        conv = getattr(torch.backends.cudnn, "conv", None)
+        self._saved = (conv.fp32_precision, torch.backends.cuda.matmul.fp32_precision) if conv is not None else \
+            (torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32)
+        if conv is not None:
+            conv.fp32_precision = "ieee"
+            torch.backends.cuda.matmul.fp32_precision = "ieee"
+        else:
+            torch.backends.cudnn.allow_tf32 = torch.backends.cuda.matmul.allow_tf32 = False
+        return self
+
+    def __exit__(self, *exc):
+        conv = getattr(torch.backends.cudnn, "conv", None)
+        if conv is not None:
+            conv.fp32_precision, torch.backends.cuda.matmul.fp32_precision = self._saved
+        else:
+            torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32 = self._saved
+        return False
+
+
 def _stages(cfg: BenchConfig, algorithm: str, x, f, plan: TilePlan | None):
     """(transform, compute, output) callables for one algorithm; buffers allocated once."""
     p = cfg.params
@@ -105,21 +128,23 @@ def _stages(cfg: BenchConfig, algorithm: str, x, f, plan: TilePlan | None):
         return tr, cv, out
     if algorithm in ("im2win-tf32", "im2win-bf16"):
         variant = algorithm[7:]
-        xc = torch.empty((cfg.batch, cfg.h_in, cfg.w_in, nhwc_pitch(cfg.c_in, variant)), device=x.device,
-                         dtype=torch.bfloat16 if variant == "bf16" else torch.float32)
-        return (lambda: nhwc_into(x, xc)), (lambda: conv_fused_into(xc, f, out, p, variant)), out
+        xc = torch.empty((cfg.batch, cfg.h_in + 2 * p.pad, cfg.w_in + 2 * p.pad, nhwc_pitch(cfg.c_in, variant)),
+                         device=x.device, dtype=torch.bfloat16 if variant == "bf16" else torch.float32)
+        return (lambda: nhwc_into(x, xc, p.pad)), (lambda: conv_fused_into(xc, f, out, p, variant)), out
     if algorithm == "cudnn":
         def cv():
-            out.copy_(F.conv2d(x, f, stride=cfg.stride))
+            with _IeeeFp32():
+                out.copy_(F.conv2d(x, f, stride=cfg.stride, padding=p.pad))
         return (lambda: None), cv, out
     if algorithm == "im2col-cublas":
         cols = {}
 
         def tr():
-            cols["c"] = F.unfold(x, (cfg.h_f, cfg.w_f), stride=cfg.stride)
+            cols["c"] = F.unfold(x, (cfg.h_f, cfg.w_f), stride=cfg.stride, padding=p.pad)
 
         def cv():
-            torch.matmul(f.view(cfg.c_out, -1), cols["c"], out=out.view(cfg.batch, cfg.c_out, -1))
+            with _IeeeFp32():
+                torch.matmul(f.view(cfg.c_out, -1), cols["c"], out=out.view(cfg.batch, cfg.c_out, -1))
         return tr, cv, out
     raise ValueError(f"unknown algorithm {algorithm!r}, expected one of {ALGORITHMS}")
 
