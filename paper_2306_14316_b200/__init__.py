@@ -22,6 +22,7 @@ from .tensors import ConvParams, Tensor4, check_conv_operands, max_rel_diff, nor
 from .plan import GemmDims, TilePlan, compose_k, compose_n, decompose_k, decompose_n, default_plan, gpu_plan
 from .layouts import Im2winTensor, effective_width, footprint_elems, im2win, im2win_gather
 from .kernels import (
+    CapturedConv,
     compute_from_windows_basic,
     compute_from_windows_opt,
     conv_im2win_basic,
@@ -39,6 +40,7 @@ VARIANTS = ("fp32-exact", "fp32-fma", "tf32", "bf16")
 __all__ = [
     "BENCHMARKS",
     "BenchConfig",
+    "CapturedConv",
     "ConvParams",
     "FixtureFormatError",
     "GemmDims",

@@ -364,3 +364,82 @@ def conv_im2win_opt_host_batch(jobs, *, variant: str = "fp32-exact", outs=None, 
         handles[i] = conv_im2win_opt_host(inp, flt, params, variant=variant, chunk_images=chunk_images,
                                           out=None if outs is None else outs[i], device=device, wait=False)
     return [h.wait() for h in handles]
+
+
+class CapturedConv:
+    """A fixed-shape im2win convolution captured once in a CUDA graph and replayed.
+
+    For serving loops that call the same layer repeatedly: the transform (or the
+    channels-last copy) and the convolution are recorded with their buffers,
+    workspace and tensor maps, so each call is one graph launch instead of several
+    Python -> C ABI -> kernel launches.  Call with a new input (and optionally a new
+    filter) of the captured shapes; the result is written into `self.out` (a device
+    tensor reused across calls; clone it to keep it).  Bit-identical to
+    `conv_im2win_opt` with the same arguments.
+    """
+
+    def __init__(self, input_shape, params: ConvParams, flt=None, plan: TilePlan | None = None, *,
+                 variant: str = "fp32-exact", device=None):
+        n_img, c_in, h_in, w_in = (int(d) for d in input_shape)
+        if c_in != params.c_in:
+            raise ShapeError(f"input has {c_in} channels, params expect {params.c_in}")
+        _variant_code(variant)
+        if not torch.cuda.is_available():
+            raise ShapeError("a CUDA device is required (this package has no CPU path)")
+        self.device = torch.device(device) if device is not None else torch.device("cuda",
+                                                                                    torch.cuda.current_device())
+        self.params, self.variant = params, variant
+        h_out, w_out = output_dims(h_in, w_in, params)
+        dev = self.device
+        self.input = torch.zeros((n_img, c_in, h_in, w_in), dtype=DTYPE, device=dev)
+        self.filter = torch.zeros(params.filter_dims, dtype=DTYPE, device=dev)
+        if flt is not None:
+            self.filter.copy_(Tensor4(flt).data)
+        self.out = torch.empty((n_img, params.c_out, h_out, w_out), dtype=DTYPE, device=dev)
+        if variant in ("tf32", "bf16"):
+            dt = torch.bfloat16 if variant == "bf16" else torch.float32
+            pad = params.pad
+            self._mid = torch.empty((n_img, h_in + 2 * pad, w_in + 2 * pad, nhwc_pitch(c_in, variant)), dtype=dt,
+                                    device=dev)
+
+            def body():
+                nhwc_into(self.input, self._mid, pad)
+                conv_fused_into(self._mid, self.filter, self.out, params, variant)
+        else:
+            from .layouts import effective_width, im2win_into
+
+            w_eff = effective_width(w_out, params.w_f, params.stride)
+            self._mid = torch.empty((n_img, c_in, h_out, params.h_f * w_eff), dtype=DTYPE, device=dev)
+
+            def body():
+                im2win_into(self.input, self._mid, params)
+                conv_windows_into(self._mid, self.filter, self.out, params, w_eff, plan, variant)
+
+        # warm up on a side stream (allocates the workspace, sets kernel attributes), then capture
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.device(dev), torch.cuda.stream(side):
+            body()
+            self.kernel = _lib.last_kernel()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=side, capture_error_mode="relaxed"):
+                body()
+        torch.cuda.current_stream(dev).wait_stream(side)
+
+    def __call__(self, inp, flt=None) -> Tensor4:
+        """Copy the operands into the captured buffers and replay (on the current stream)."""
+        x = inp.data if isinstance(inp, Tensor4) else inp
+        if not isinstance(x, torch.Tensor):
+            x = Tensor4(x).data
+        if tuple(x.shape) != tuple(self.input.shape):
+            raise ShapeError(f"input shape {tuple(x.shape)} differs from the captured {tuple(self.input.shape)}")
+        self.input.copy_(x, non_blocking=True)
+        if flt is not None:
+            fd = flt.data if isinstance(flt, Tensor4) else flt
+            if not isinstance(fd, torch.Tensor):
+                fd = Tensor4(fd).data
+            if tuple(fd.shape) != tuple(self.filter.shape):
+                raise ShapeError(f"filter dims {tuple(fd.shape)} do not match params {self.params.filter_dims}")
+            self.filter.copy_(fd, non_blocking=True)
+        self.graph.replay()
+        return Tensor4(self.out)

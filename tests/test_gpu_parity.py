@@ -444,3 +444,19 @@ def test_host_batch_api_order_and_bits():
     outs = pkg.conv_im2win_opt_host_batch(jobs)
     for (inp, flt, params), out in zip(jobs, outs):
         assert bits_equal(out.numpy(), pkg.conv_im2win_opt(inp, flt, params).numpy())
+
+
+@pytest.mark.parametrize("variant", pkg.VARIANTS)
+def test_captured_conv_replays_bitwise(variant):
+    """CapturedConv (CUDA-graph replay) equals conv_im2win_opt bit for bit, for new inputs and
+    a new filter on every replay, including a padded geometry."""
+    for name, pad in (("conv10", 0), ("conv9", 1)):
+        cfg = replace(BENCHMARKS[name], batch=3)
+        params = pkg.ConvParams(cfg.c_in, cfg.c_out, cfg.h_f, cfg.w_f, cfg.stride, pad=pad)
+        cap = pkg.CapturedConv((3, cfg.c_in, cfg.h_in, cfg.w_in), params, variant=variant)
+        for seed in (1, 2):
+            inp, flt = make_inputs(replace(cfg, seed=seed))
+            got = cap(torch.from_numpy(inp).to(DEV), torch.from_numpy(flt).to(DEV)).numpy()
+            tc = "fused" if variant in ("tf32", "bf16") else "auto"
+            ref = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path=tc).numpy()
+            assert bits_equal(got, ref), (name, pad, seed)
