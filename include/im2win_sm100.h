@@ -129,6 +129,25 @@ int im2win_conv_fused(const void* x_nhwc, const float* flt, float* out, int64_t 
                       int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
                       int32_t variant, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Direct tensor-core path for few-channel inputs (extension) ----
+ * For C <= 16 (the RGB input layers) producer warps build each output pixel's im2win
+ * window (k = (c, fh, fw), C*Hf*Wf values) from an input patch staged in shared memory
+ * and feed tcgen05 directly: no channels-last copy, no TMA window boxes.  x is the NCHW
+ * float32 input; pad zero-pads it on every side.  variant = IM2WIN_TF32 or IM2WIN_BF16.
+ * im2win_conv_direct_supported returns 1 when the shape fits (else use the fused path). */
+int32_t im2win_conv_direct_supported(int64_t n, int64_t c_in, int64_t h, int64_t w, int64_t c_out,
+                                     int32_t h_f, int32_t w_f, int32_t stride, int32_t pad, int32_t variant);
+
+/* 1 when the library's automatic path would pick the direct kernel over copy + fused. */
+int32_t im2win_conv_direct_preferred(int64_t n, int64_t c_in, int64_t h, int64_t w, int64_t c_out,
+                                     int32_t h_f, int32_t w_f, int32_t stride, int32_t pad, int32_t variant);
+
+size_t im2win_conv_direct_workspace(int64_t c_in, int64_t c_out, int32_t h_f, int32_t w_f, int32_t variant);
+
+int im2win_conv_direct(const float* x, const float* flt, float* out, int64_t n, int64_t c_in, int64_t h,
+                       int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride, int32_t pad,
+                       int32_t variant, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- Host-buffer entry point (extension of conv_im2win_opt, optimized.py:237-241) ----
  * The reference is called with host (numpy) operands and returns a host array.
  * This runs transform + conv over host buffers: the batch is cut into chunks of

@@ -41,6 +41,10 @@ EXPORTED_SYMBOLS = (
     "im2win_conv_fused_workspace_bytes",
     "im2win_conv_fused",
     "im2win_conv_basic_f32",
+    "im2win_conv_direct_supported",
+    "im2win_conv_direct_preferred",
+    "im2win_conv_direct_workspace",
+    "im2win_conv_direct",
     "im2win_conv_host_workspace_bytes",
     "im2win_conv_host_f32",
     "im2win_conv_host_submit",
@@ -109,6 +113,14 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         lib.im2win_conv_fused.restype = ctypes.c_int
         lib.im2win_conv_basic_f32.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i32, i32, i32, vp]
         lib.im2win_conv_basic_f32.restype = ctypes.c_int
+        lib.im2win_conv_direct_supported.argtypes = [i64, i64, i64, i64, i64, i32, i32, i32, i32, i32]
+        lib.im2win_conv_direct_supported.restype = ctypes.c_int32
+        lib.im2win_conv_direct_preferred.argtypes = [i64, i64, i64, i64, i64, i32, i32, i32, i32, i32]
+        lib.im2win_conv_direct_preferred.restype = ctypes.c_int32
+        lib.im2win_conv_direct_workspace.argtypes = [i64, i64, i32, i32, i32]
+        lib.im2win_conv_direct_workspace.restype = sz
+        lib.im2win_conv_direct.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32, i32, i32, vp, sz, vp]
+        lib.im2win_conv_direct.restype = ctypes.c_int
         lib.im2win_conv_host_workspace_bytes.argtypes = [i64, i64, i64, i64, i64, i32, i32, i32, i32, i32, i64]
         lib.im2win_conv_host_workspace_bytes.restype = sz
         lib.im2win_conv_host_f32.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32, i32,

@@ -17,7 +17,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libim2win_sm100.so"
-SOURCES = ["capi.cu", "transform.cu", "conv_simt.cu", "conv_tc.cu", "conv_tc_cl.cu", "conv_tc_fused.cu", "conv_tc_shift.cu", "conv_tc_phase.cu", "peak.cu", "pipeline.cu"]
+SOURCES = ["capi.cu", "transform.cu", "conv_simt.cu", "conv_tc.cu", "conv_tc_cl.cu", "conv_tc_fused.cu", "conv_tc_shift.cu", "conv_tc_phase.cu", "conv_tc_direct.cu", "peak.cu", "pipeline.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -258,3 +258,56 @@ extern "C" int im2win_conv_basic_f32(const float* windows, const float* flt, flo
                                     static_cast<cudaStream_t>(stream), &err);
   return rc ? fail(rc, err) : 0;
 }
+
+// ---- direct tensor-core path for few-channel inputs (conv_tc_direct.cu) ----
+int im2win_conv_direct_applies(int64_t n, int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f,
+                               int stride, int pad, int bf16);
+size_t im2win_conv_direct_workspace_bytes(int64_t c_in, int64_t c_out, int h_f, int w_f, int bf16);
+int im2win_launch_conv_tc_direct(const float* x, const float* flt, float* out, void* workspace, size_t ws_bytes,
+                                 int64_t n, int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f,
+                                 int stride, int pad, int bf16, cudaStream_t stream, const char** err);
+
+extern "C" {
+
+int32_t im2win_conv_direct_supported(int64_t n, int64_t c_in, int64_t h, int64_t w, int64_t c_out, int32_t h_f,
+                                     int32_t w_f, int32_t stride, int32_t pad, int32_t variant) {
+  if (variant != IM2WIN_TF32 && variant != IM2WIN_BF16) return 0;
+  if (n < 1 || c_in < 1 || h < 1 || w < 1 || c_out < 1 || h_f < 1 || w_f < 1 || stride < 1) return 0;
+  return im2win_conv_direct_applies(n, c_in, h, w, c_out, h_f, w_f, stride, pad, variant == IM2WIN_BF16);
+}
+
+// The library's automatic choice between the direct kernel and channels-last copy + fused
+// kernel (used by conv_im2win_opt(tc_path="auto"), CapturedConv and the host pipeline).
+// Measured on B200 (tools/tc_kernels.py, N=128, copy + conv): direct wins for BF16 when the
+// fused kernel's window boxes are short -- several output rows per tile (w_out <= 64: 11x11
+// stride-4 layers) or a tiny window (K <= 32) -- and loses elsewhere (7x7 stride 2; TF32).
+int32_t im2win_conv_direct_preferred(int64_t n, int64_t c_in, int64_t h, int64_t w, int64_t c_out, int32_t h_f,
+                                     int32_t w_f, int32_t stride, int32_t pad, int32_t variant) {
+  if (variant != IM2WIN_BF16) return 0;
+  if (!im2win_conv_direct_supported(n, c_in, h, w, c_out, h_f, w_f, stride, pad, variant)) return 0;
+  const int64_t w_out = (w + 2 * pad - w_f) / stride + 1;
+  return (w_out <= 64 || c_in * h_f * w_f <= 32) ? 1 : 0;
+}
+
+size_t im2win_conv_direct_workspace(int64_t c_in, int64_t c_out, int32_t h_f, int32_t w_f, int32_t variant) {
+  return im2win_conv_direct_workspace_bytes(c_in, c_out, h_f, w_f, variant == IM2WIN_BF16);
+}
+
+int im2win_conv_direct(const float* x, const float* flt, float* out, int64_t n, int64_t c_in, int64_t h, int64_t w,
+                       int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride, int32_t pad, int32_t variant,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_error[0] = '\0';
+  if (!x || !flt || !out || !workspace) return fail(1, "im2win_conv_direct: null pointer");
+  if (variant != IM2WIN_TF32 && variant != IM2WIN_BF16)
+    return fail(1, "im2win_conv_direct: variant must be IM2WIN_TF32 or IM2WIN_BF16");
+  if (n < 1 || c_in < 1 || h < 1 || w < 1 || c_out < 1 || h_f < 1 || w_f < 1 || stride < 1 || pad < 0)
+    return fail(1, "im2win_conv_direct: extents must be positive");
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return fail(1, "im2win_conv_direct: workspace alignment");
+  if (int rc = bind_device_of(out)) return rc;
+  const char* err = nullptr;
+  int rc = im2win_launch_conv_tc_direct(x, flt, out, workspace, workspace_bytes, n, c_in, h, w, c_out, h_f, w_f,
+                                        stride, pad, variant == IM2WIN_BF16, static_cast<cudaStream_t>(stream), &err);
+  return rc ? fail(rc, err) : 0;
+}
+
+}  // extern "C"

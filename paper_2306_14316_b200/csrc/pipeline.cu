@@ -51,7 +51,7 @@ DevPipe g_pipes[kMaxDev];
 struct Geometry {
   int64_t n, c_in, h, w, c_out, h_out, w_out, w_eff;
   int h_f, w_f, stride, pad;
-  bool tc;
+  bool tc, direct;  // direct: the few-channel TC kernel reads the NCHW chunk itself
   int64_t pitch;  // channels-last pitch for the TC path
   size_t in_elems, mid_bytes, out_elems, flt_elems, conv_ws;
 };
@@ -79,7 +79,11 @@ Geometry geometry(int64_t n_chunk, int64_t c_in, int64_t h, int64_t w, int64_t c
   g.in_elems = static_cast<size_t>(n_chunk * c_in * h * w);
   g.out_elems = static_cast<size_t>(n_chunk * c_out * g.h_out * g.w_out);
   g.flt_elems = static_cast<size_t>(c_out * c_in * h_f * w_f);
-  if (g.tc) {
+  g.direct = g.tc && im2win_conv_direct_preferred(n_chunk, c_in, h, w, c_out, h_f, w_f, stride, pad, variant);
+  if (g.direct) {
+    g.mid_bytes = 0;
+    g.conv_ws = im2win_conv_direct_workspace(c_in, c_out, h_f, w_f, variant);
+  } else if (g.tc) {
     g.mid_bytes = static_cast<size_t>(n_chunk * (h + 2 * pad) * (w + 2 * pad) * g.pitch) * (variant == IM2WIN_BF16 ? 2 : 4);
     g.conv_ws = im2win_conv_fused_workspace_bytes(c_in, c_out, h_f, w_f);
   } else {
@@ -210,7 +214,12 @@ static int host_conv(const float* host_in, const float* host_flt, float* host_ou
     // compute (output buffer s was last read by chunk k-2's download)
     cudaStreamWaitEvent(P.comp, P.in_ready[s], 0);
     if (k >= D) cudaStreamWaitEvent(P.comp, P.out_done[s], 0);
-    if (g.tc) {
+    if (g.direct) {
+      // the direct kernel reads the chunk's NCHW input itself: buffer s is free once it finishes
+      rc = im2win_conv_direct(d_in[s], d_flt, d_out[s], nk, c_in, h, w, c_out, h_f, w_f, stride, pad, variant,
+                              conv_ws, g.conv_ws, P.comp);
+      cudaEventRecord(P.xf_done[s], P.comp);
+    } else if (g.tc) {
       rc = im2win_nchw_to_nhwc_padded(d_in[s], mid, nk, c_in, h, w, variant == IM2WIN_BF16 ? 1 : 0, pad, P.comp);
       cudaEventRecord(P.xf_done[s], P.comp);
       if (!rc)

@@ -199,7 +199,42 @@ def conv_fused_into(x_nhwc: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, 
     _lib.check(rc)
 
 
-TC_PATHS = ("auto", "fused", "cl", "gather")
+def direct_supported(inp_dims, params: ConvParams, variant: str) -> bool:
+    """Whether the in-SM im2win tensor-core kernel (few-channel inputs) covers this shape."""
+    if variant not in ("tf32", "bf16"):
+        return False
+    n_img, c_in, h_in, w_in = (int(d) for d in inp_dims)
+    return bool(_lib.load().im2win_conv_direct_supported(n_img, c_in, h_in, w_in, params.c_out, params.h_f,
+                                                         params.w_f, params.stride, params.pad,
+                                                         _variant_code(variant)))
+
+
+def direct_preferred(inp_dims, params: ConvParams, variant: str) -> bool:
+    """The auto path's choice of the direct kernel (library rule im2win_conv_direct_preferred)."""
+    if variant not in ("tf32", "bf16"):
+        return False
+    n_img, c_in, h_in, w_in = (int(d) for d in inp_dims)
+    return bool(_lib.load().im2win_conv_direct_preferred(n_img, c_in, h_in, w_in, params.c_out, params.h_f,
+                                                         params.w_f, params.stride, params.pad,
+                                                         _variant_code(variant)))
+
+
+def conv_direct_into(x: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, params: ConvParams, variant: str) -> None:
+    """tcgen05 convolution that builds the im2win windows in shared memory from the NCHW input."""
+    n_img, c_in, h_in, w_in = (int(d) for d in x.shape)
+    code = _variant_code(variant)
+    lib = _lib.load()
+    nbytes = lib.im2win_conv_direct_workspace(c_in, params.c_out, params.h_f, params.w_f, code)
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    ws = _workspace(out.device, stream, nbytes)
+    with torch.cuda.device(out.device):
+        rc = lib.im2win_conv_direct(x.data_ptr(), flt.data_ptr(), out.data_ptr(), n_img, c_in, h_in, w_in,
+                                    params.c_out, params.h_f, params.w_f, params.stride, params.pad, code,
+                                    ws.data_ptr(), ws.numel(), stream)
+    _lib.check(rc)
+
+
+TC_PATHS = ("auto", "direct", "fused", "cl", "gather")
 
 
 def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, *,
@@ -207,7 +242,9 @@ def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, 
     """Window-order transform followed by the tiled kernel (optimized.py:237-241).
 
     FP32 variants use the reference window layout Ĩ.  Tensor-core variants pick
-    (tc_path="auto"): "fused" — TMA builds window tiles from a channels-last copy
+    (tc_path="auto"): "direct" — for few-channel inputs (C <= 16) producer warps
+    build each pixel's im2win window in shared memory from the NCHW input;
+    "fused" — TMA builds window tiles from a channels-last copy
     of the input (no Ĩ); "cl" — materialised channels-innermost Ĩ streamed by TMA;
     "gather" — reference Ĩ gathered by producer warps.  The fused copy pads the
     channel pitch to a 16-byte multiple (zeros); "cl" needs c_in * element size
@@ -219,8 +256,15 @@ def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, 
     f = flt if isinstance(flt, Tensor4) else Tensor4(flt)
     h_out, w_out = check_conv_operands(i, f, params)
     ok = cl_supported(params.c_in, variant)
-    if tc_path == "auto" and variant == "tf32" and not ok:
-        tc_path = "gather"  # measured: for C*4 % 16 != 0 (C=3 layers) the gathered Ĩ beats the padded copy
+    use_direct = direct_supported(i.dims, params, variant) if tc_path == "direct" else (
+        tc_path == "auto" and direct_preferred(i.dims, params, variant))
+    if use_direct:
+        out = torch.empty((i.dims[0], params.c_out, h_out, w_out), dtype=DTYPE, device=i.device)
+        fd = f.data if f.device == i.device else f.data.to(i.device)
+        conv_direct_into(i.data, fd, out, params, variant)
+        return Tensor4(out)
+    if tc_path == "direct":
+        raise ValueError("tc_path='direct' does not cover this shape (needs C <= 16, Co <= 256)")
     if variant in ("tf32", "bf16") and tc_path in ("auto", "fused"):
         dt = torch.bfloat16 if variant == "bf16" else torch.float32
         n_img, c_in, h_in, w_in = i.dims
@@ -396,7 +440,10 @@ class CapturedConv:
         if flt is not None:
             self.filter.copy_(Tensor4(flt).data)
         self.out = torch.empty((n_img, params.c_out, h_out, w_out), dtype=DTYPE, device=dev)
-        if variant in ("tf32", "bf16"):
+        if variant in ("tf32", "bf16") and direct_preferred(self.input.shape, params, variant):
+            def body():
+                conv_direct_into(self.input, self.filter, self.out, params, variant)
+        elif variant in ("tf32", "bf16"):
             dt = torch.bfloat16 if variant == "bf16" else torch.float32
             pad = params.pad
             self._mid = torch.empty((n_img, h_in + 2 * pad, w_in + 2 * pad, nhwc_pitch(c_in, variant)), dtype=dt,

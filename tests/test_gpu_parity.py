@@ -283,7 +283,7 @@ def test_host_pipeline_equals_device_path(variant):
     cfg = replace(BENCHMARKS["conv10"], batch=11, seed=5)
     inp, flt = make_inputs(cfg)
     if variant in ("tf32", "bf16"):
-        dev = pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant, tc_path="fused").numpy()
+        dev = pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant).numpy()
     else:
         dev = pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant).numpy()
     pinned_in = torch.from_numpy(inp).pin_memory()
@@ -423,10 +423,11 @@ def test_native_padding_tensor_cores(variant):
         flt = rng.standard_normal((co, c, hf, wf), dtype=np.float32)
         params = pkg.ConvParams(c, co, hf, wf, s, pad=p)
         ref = orc.conv_direct(_pad_np(inp, p), flt, s)
-        for path in ("fused", "gather"):
+        paths = ("fused", "gather") + (("direct",) if c <= 16 else ())
+        for path in paths:
             out = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path=path).numpy()
             assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (n, c, h, w, p, path)
-        dev = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path="fused").numpy()
+        dev = pkg.conv_im2win_opt(inp, flt, params, variant=variant).numpy()
         host = pkg.conv_im2win_opt_host(inp, flt, params, variant=variant, chunk_images=1).numpy()
         assert bits_equal(host, dev)
     with pytest.raises(ValueError):
@@ -457,6 +458,43 @@ def test_captured_conv_replays_bitwise(variant):
         for seed in (1, 2):
             inp, flt = make_inputs(replace(cfg, seed=seed))
             got = cap(torch.from_numpy(inp).to(DEV), torch.from_numpy(flt).to(DEV)).numpy()
-            tc = "fused" if variant in ("tf32", "bf16") else "auto"
-            ref = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path=tc).numpy()
+            ref = pkg.conv_im2win_opt(inp, flt, params, variant=variant).numpy()
             assert bits_equal(got, ref), (name, pad, seed)
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_tc_direct_layers(variant, layer_goldens):
+    """The in-SM im2win tensor-core kernel on every few-channel benchmark layer (conv1-3, conv7)."""
+    for name in ("conv1", "conv2", "conv3", "conv7"):
+        g = layer_goldens[name]
+        cfg = replace(BENCHMARKS[name], batch=g["batch"], seed=g["seed"])
+        inp, flt = make_inputs(cfg)
+        ref = orc.conv_direct(inp, flt, cfg.stride)
+        out = pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant, tc_path="direct").numpy()
+        assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], name
+        from paper_2306_14316_b200 import _lib
+        assert "conv_tc_direct_kernel" in _lib.last_kernel()
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_tc_direct_geometries(variant):
+    """Direct kernel on ragged geometries: C 1..16, strides 1-4, filters up to 11x11, padding,
+    multi-row tiles, split rows (w_out > 128), one image and odd batch counts."""
+    cases = [(1, 1, 9, 7, 16, 3, 3, 1, 0), (3, 3, 40, 300, 64, 5, 5, 2, 2), (2, 4, 31, 33, 96, 11, 11, 4, 0),
+             (2, 8, 17, 17, 128, 7, 7, 2, 3), (1, 16, 12, 12, 256, 3, 3, 1, 1), (5, 3, 20, 20, 64, 3, 3, 1, 1),
+             (1, 2, 8, 140, 32, 1, 1, 1, 0)]
+    for (n, c, h, w, co, hf, wf, s, p) in cases:
+        rng = np.random.default_rng(n + c + h + w)
+        inp = rng.standard_normal((n, c, h, w), dtype=np.float32)
+        flt = rng.standard_normal((co, c, hf, wf), dtype=np.float32)
+        ref = orc.conv_direct(_pad_np(inp, p), flt, s)
+        params = pkg.ConvParams(c, co, hf, wf, s, pad=p)
+        if not pkg.kernels.direct_supported(inp.shape, params, variant):
+            # tf32 with a large window: the resident filter would not fit; auto uses the fused path
+            assert variant == "tf32", (n, c, h, w, co, hf, wf, s, p)
+            with pytest.raises(ValueError):
+                pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path="direct")
+            out = pkg.conv_im2win_opt(inp, flt, params, variant=variant).numpy()
+        else:
+            out = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path="direct").numpy()
+        assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (n, c, h, w, co, hf, wf, s, p)

@@ -13,7 +13,13 @@ import torch  # noqa: E402
 
 import paper_2306_14316_b200 as pkg  # noqa: E402
 from oracle import oracle as orc  # noqa: E402
-from paper_2306_14316_b200.kernels import conv_fused_into, nhwc_into, nhwc_pitch  # noqa: E402
+from paper_2306_14316_b200.kernels import (  # noqa: E402
+    conv_direct_into,
+    conv_fused_into,
+    direct_supported,
+    nhwc_into,
+    nhwc_pitch,
+)
 
 layers = sys.argv[1].split(",") if len(sys.argv) > 1 and sys.argv[1] != "all" else list(pkg.BENCHMARKS)
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 128
@@ -58,6 +64,11 @@ for name in layers:
                 pkg.conv_im2win_opt(inp, flt, c2.params, variant=v, tc_path="fused").numpy(), ref)
             t = timed(lambda: conv_fused_into(xc, f, o, cb.params, v))
             row.append(f"{sel} {cb.flops / t / 1e9:7.1f} TF (err {err:.1e})")
+        if direct_supported(x.shape, cb.params, v):
+            err = pkg.normalized_max_diff(
+                pkg.conv_im2win_opt(inp, flt, c2.params, variant=v, tc_path="direct").numpy(), ref)
+            t = timed(lambda: conv_direct_into(x, f, o, cb.params, v))
+            row.append(f"direct {cb.flops / t / 1e9:7.1f} TF (err {err:.1e}, no NHWC copy)")
         print("  ".join(row), flush=True)
         del x, f, o, xc
         torch.cuda.empty_cache()
