@@ -1,0 +1,171 @@
+// Does the TC epilogue's NCHW store pattern (lane = pixel, one 4-byte store per channel,
+// tiles of box_w pixels x 64 channels) limit conv7-shaped outputs?  Writes N x 64 x 222 x 222
+// fp32 with that pattern from 148 persistent CTAs (warps = lane quarters x column halves,
+// as in the kernels), and with a plain grid-stride float4 fill, and reports TB/s.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o nchw_store_probe nchw_store_probe.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void __launch_bounds__(256) pattern(float* out, int n, int co, int ho, int wo, int box_w, int warps_per_tile) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int quarter = warp % 4, half = warp / 4;  // 8 warps: 4 lane quarters x 2 column halves
+  const int ow_tiles = (wo + box_w - 1) / box_w;
+  const long long tiles = (long long)n * ho * ow_tiles;
+  const int r = quarter * 32 + lane;
+  const long long hw = (long long)ho * wo;
+  for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int owt = t % ow_tiles;
+    const long long rest = t / ow_tiles;
+    const int oh = rest % ho;
+    const long long img = rest / ho;
+    const int ow = owt * box_w + r;
+    if (r < box_w && ow < wo) {
+      float* base = out + img * co * hw + (long long)oh * wo + ow;
+      const int c0 = half * (co / 2);
+#pragma unroll 8
+      for (int c = 0; c < co / 2; ++c) base[(long long)(c0 + c) * hw] = (float)c;
+    }
+  }
+}
+
+// Variant: plane stride padded by `pad_elems` floats (is it L2/DRAM address aliasing of the 64 planes?)
+__global__ void __launch_bounds__(256) pattern_pad(float* out, int n, int co, int ho, int wo, int box_w, long long plane) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int quarter = warp % 4, half = warp / 4;
+  const int ow_tiles = (wo + box_w - 1) / box_w;
+  const long long tiles = (long long)n * ho * ow_tiles;
+  const int r = quarter * 32 + lane;
+  for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int owt = t % ow_tiles;
+    const long long rest = t / ow_tiles;
+    const int oh = rest % ho;
+    const long long img = rest / ho;
+    const int ow = owt * box_w + r;
+    if (r < box_w && ow < wo) {
+      float* base = out + img * co * plane + (long long)oh * wo + ow;
+      const int c0 = half * (co / 2);
+#pragma unroll 8
+      for (int c = 0; c < co / 2; ++c) base[(long long)(c0 + c) * plane] = (float)c;
+    }
+  }
+}
+
+// Variant: each warp writes one plane's 128-pixel run per step with 4 consecutive pixels per lane
+__global__ void __launch_bounds__(256) pattern_runs(float* out, int n, int co, int ho, int wo, int box_w) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int ow_tiles = (wo + box_w - 1) / box_w;
+  const long long tiles = (long long)n * ho * ow_tiles;
+  const long long hw = (long long)ho * wo;
+  for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int owt = t % ow_tiles;
+    const long long rest = t / ow_tiles;
+    const int oh = rest % ho;
+    const long long img = rest / ho;
+    for (int c = warp; c < co; c += 8) {
+      float* base = out + (img * co + c) * hw + (long long)oh * wo + owt * box_w;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int px = q * 32 + lane;
+        if (px < box_w && owt * box_w + px < wo) base[px] = (float)c;
+      }
+    }
+  }
+}
+
+// Variant: a "tile" is `rows_per` full output rows; each warp writes one plane's contiguous run
+// of rows_per * wo pixels (NCHW rows are contiguous within a plane).
+__global__ void __launch_bounds__(256) pattern_rowruns(float* out, int n, int co, int ho, int wo, int rows_per) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int oh_tiles = (ho + rows_per - 1) / rows_per;
+  const long long tiles = (long long)n * oh_tiles;
+  const long long hw = (long long)ho * wo;
+  for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int oh0 = (t % oh_tiles) * rows_per;
+    const long long img = t / oh_tiles;
+    const int run = min(rows_per, ho - oh0) * wo;
+    for (int c = warp; c < co; c += 8) {
+      float* base = out + (img * co + c) * hw + (long long)oh0 * wo;
+      for (int px = lane; px < run; px += 32) base[px] = (float)c;
+    }
+  }
+}
+
+__global__ void fill(float4* out, long long n4) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x)
+    out[i] = make_float4(1.f, 2.f, 3.f, 4.f);
+}
+
+int main() {
+  const int n = 128, co = 64, ho = 222, wo = 222;
+  const size_t elems = (size_t)n * co * ho * wo;
+  float* out;
+  cudaMalloc(&out, elems * 4);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int box_w : {111, 128, 74}) {
+    pattern<<<148, 256>>>(out, n, co, ho, wo, box_w, 8);
+    cudaEventRecord(e0);
+    pattern<<<148, 256>>>(out, n, co, ho, wo, box_w, 8);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("pattern box_w=%d: %.3f ms  %.2f TB/s\n", box_w, ms, elems * 4 / (ms * 1e-3) / 1e12);
+  }
+  for (int ctas : {148, 148 * 2, 148 * 8}) {
+    pattern<<<ctas, 256>>>(out, n, co, ho, wo, 111, 8);
+    cudaEventRecord(e0);
+    pattern<<<ctas, 256>>>(out, n, co, ho, wo, 111, 8);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("pattern ctas=%d: %.3f ms  %.2f TB/s\n", ctas, ms, elems * 4 / (ms * 1e-3) / 1e12);
+  }
+  {
+    const long long plane = (long long)ho * wo;
+    float* out2;
+    cudaMalloc(&out2, ((size_t)n * co * (plane + 64)) * 4);
+    for (long long pad : {0LL, 32LL, 64LL}) {
+      pattern_pad<<<148, 256>>>(out2, n, co, ho, wo, 111, plane + pad);
+      cudaEventRecord(e0);
+      pattern_pad<<<148, 256>>>(out2, n, co, ho, wo, 111, plane + pad);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("pattern plane+%lld: %.3f ms  %.2f TB/s\n", pad, ms, elems * 4 / (ms * 1e-3) / 1e12);
+    }
+    cudaFree(out2);
+  }
+  for (int box_w : {111, 128}) {
+    pattern_runs<<<148, 256>>>(out, n, co, ho, wo, box_w);
+    cudaEventRecord(e0);
+    pattern_runs<<<148, 256>>>(out, n, co, ho, wo, box_w);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("runs box_w=%d: %.3f ms  %.2f TB/s\n", box_w, ms, elems * 4 / (ms * 1e-3) / 1e12);
+  }
+  for (int rp : {1, 2, 4, 8}) {
+    pattern_rowruns<<<148, 256>>>(out, n, co, ho, wo, rp);
+    cudaEventRecord(e0);
+    pattern_rowruns<<<148, 256>>>(out, n, co, ho, wo, rp);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("rowruns rows=%d: %.3f ms  %.2f TB/s\n", rp, ms, elems * 4 / (ms * 1e-3) / 1e12);
+  }
+  fill<<<148 * 8, 256>>>((float4*)out, elems / 4);
+  cudaEventRecord(e0);
+  fill<<<148 * 8, 256>>>((float4*)out, elems / 4);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("float4 fill: %.3f ms  %.2f TB/s\n", ms, elems * 4 / (ms * 1e-3) / 1e12);
+  return 0;
+}
