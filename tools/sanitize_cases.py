@@ -1,0 +1,35 @@
+"""Small invocations of every kernel family, for compute-sanitizer runs:
+
+    compute-sanitizer --tool memcheck python tools/sanitize_cases.py
+    compute-sanitizer --tool racecheck python tools/sanitize_cases.py
+    compute-sanitizer --tool synccheck python tools/sanitize_cases.py
+"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2306_14316_b200 as pkg  # noqa: E402
+
+rng = np.random.default_rng(0)
+cases = [(2, 3, 13, 15, 16, 3, 3, 1, 0), (1, 8, 11, 9, 8, 5, 5, 2, 1), (2, 16, 10, 10, 32, 3, 3, 1, 1),
+         (1, 4, 23, 23, 96, 11, 11, 4, 0), (1, 64, 12, 12, 64, 7, 7, 2, 3)]
+for (n, c, h, w, co, hf, wf, s, p) in cases:
+    x = torch.from_numpy(rng.standard_normal((n, c, h, w), dtype=np.float32)).cuda()
+    f = torch.from_numpy(rng.standard_normal((co, c, hf, wf), dtype=np.float32)).cuda()
+    params = pkg.ConvParams(c, co, hf, wf, s, pad=p)
+    pkg.conv_im2win_opt(x, f, params)
+    pkg.conv_im2win_opt(x, f, params, variant="fp32-fma")
+    win = pkg.im2win(x, params)
+    pkg.compute_from_windows_basic(win, f, params)
+    pkg.compute_from_windows_opt(win, f, params, pkg.TilePlan(64, 64, 8, 4, 4))
+    for v in ("tf32", "bf16"):
+        for path in ("fused", "gather", "direct"):
+            if path == "direct" and not pkg.kernels.direct_supported(x.shape, params, v):
+                continue
+            pkg.conv_im2win_opt(x, f, params, variant=v, tc_path=path)
+    pkg.conv_im2win_opt_host(x.cpu(), f.cpu(), params, chunk_images=1)
+torch.cuda.synchronize()
+print("sanitize cases done")
