@@ -90,6 +90,37 @@ __global__ void __launch_bounds__(256) pattern_rowruns(float* out, int n, int co
   }
 }
 
+// Variant: the kernels' pattern with a store cache hint (0: default, 1: .cs streaming, 2: L2 evict_last)
+template <int HINT>
+__global__ void __launch_bounds__(256) pattern_hint(float* out, int n, int co, int ho, int wo, int box_w) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int quarter = warp % 4, half = warp / 4;
+  const int ow_tiles = (wo + box_w - 1) / box_w;
+  const long long tiles = (long long)n * ho * ow_tiles;
+  const int r = quarter * 32 + lane;
+  const long long hw = (long long)ho * wo;
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  for (long long t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int owt = t % ow_tiles;
+    const long long rest = t / ow_tiles;
+    const int oh = rest % ho;
+    const long long img = rest / ho;
+    const int ow = owt * box_w + r;
+    if (r < box_w && ow < wo) {
+      float* base = out + img * co * hw + (long long)oh * wo + ow;
+      const int c0 = half * (co / 2);
+#pragma unroll 8
+      for (int c = 0; c < co / 2; ++c) {
+        float* d = base + (long long)(c0 + c) * hw;
+        if (HINT == 1) __stcs(d, (float)c);
+        else if (HINT == 2) asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(d), "f"((float)c), "l"(pol) : "memory");
+        else *d = (float)c;
+      }
+    }
+  }
+}
+
 __global__ void fill(float4* out, long long n4) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x)
     out[i] = make_float4(1.f, 2.f, 3.f, 4.f);
@@ -158,6 +189,17 @@ int main() {
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     printf("rowruns rows=%d: %.3f ms  %.2f TB/s\n", rp, ms, elems * 4 / (ms * 1e-3) / 1e12);
+  }
+  {
+    float ms;
+    pattern_hint<1><<<148, 256>>>(out, n, co, ho, wo, 111);
+    cudaEventRecord(e0); pattern_hint<1><<<148, 256>>>(out, n, co, ho, wo, 111); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+    printf("pattern .cs: %.3f ms  %.2f TB/s\n", ms, elems * 4 / (ms * 1e-3) / 1e12);
+    pattern_hint<2><<<148, 256>>>(out, n, co, ho, wo, 111);
+    cudaEventRecord(e0); pattern_hint<2><<<148, 256>>>(out, n, co, ho, wo, 111); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+    printf("pattern evict_last: %.3f ms  %.2f TB/s\n", ms, elems * 4 / (ms * 1e-3) / 1e12);
   }
   fill<<<148 * 8, 256>>>((float4*)out, elems / 4);
   cudaEventRecord(e0);
