@@ -33,6 +33,13 @@ def _workspace(device: torch.device, stream: int, nbytes: int) -> torch.Tensor:
     return buf
 
 
+def _check_ws(ws: torch.Tensor, nbytes: int) -> torch.Tensor:
+    """A caller-owned workspace (e.g. one a captured CUDA graph keeps referencing)."""
+    if ws.numel() * ws.element_size() < nbytes or not ws.is_cuda:
+        raise ShapeError(f"workspace of {ws.numel() * ws.element_size()} bytes, need {nbytes}")
+    return ws
+
+
 def _variant_code(variant: str) -> int:
     try:
         return _lib.VARIANTS[variant]
@@ -41,7 +48,8 @@ def _variant_code(variant: str) -> int:
 
 
 def conv_windows_into(win: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, params: ConvParams,
-                      w_eff: int, plan: TilePlan | None = None, variant: str = "fp32-exact") -> None:
+                      w_eff: int, plan: TilePlan | None = None, variant: str = "fp32-exact",
+                      ws: torch.Tensor | None = None) -> None:
     """Launch the convolution into a caller-allocated output (the optimized.py:228-233 seam)."""
     n_img, c_in, h_out, row_len = (int(d) for d in win.shape)
     w_out = int(out.shape[3])
@@ -49,7 +57,7 @@ def conv_windows_into(win: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, p
     lib = _lib.load()
     nbytes = lib.im2win_conv_workspace_bytes(c_in, params.c_out, params.h_f, params.w_f, code)
     stream = torch.cuda.current_stream(win.device).cuda_stream
-    ws = _workspace(win.device, stream, nbytes)
+    ws = _workspace(win.device, stream, nbytes) if ws is None else _check_ws(ws, nbytes)
     cplan = to_c_plan(plan)
     with torch.cuda.device(win.device):
         rc = lib.im2win_conv_f32(
@@ -183,7 +191,7 @@ def nhwc_pitch(c_in: int, variant: str) -> int:
 
 
 def conv_fused_into(x_nhwc: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, params: ConvParams,
-                    variant: str) -> None:
+                    variant: str, ws: torch.Tensor | None = None) -> None:
     """tcgen05 convolution whose window tiles TMA builds from the channels-last input."""
     n_img, h_in, w_in, _pitch = (int(d) for d in x_nhwc.shape)
     c_in = params.c_in
@@ -191,7 +199,7 @@ def conv_fused_into(x_nhwc: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, 
     lib = _lib.load()
     nbytes = lib.im2win_conv_fused_workspace_bytes(params.c_in, params.c_out, params.h_f, params.w_f)
     stream = torch.cuda.current_stream(out.device).cuda_stream
-    ws = _workspace(out.device, stream, nbytes)
+    ws = _workspace(out.device, stream, nbytes) if ws is None else _check_ws(ws, nbytes)
     with torch.cuda.device(out.device):
         rc = lib.im2win_conv_fused(x_nhwc.data_ptr(), flt.data_ptr(), out.data_ptr(), n_img, c_in, h_in, w_in,
                                    params.c_out, params.h_f, params.w_f, params.stride, code, ws.data_ptr(),
@@ -219,14 +227,15 @@ def direct_preferred(inp_dims, params: ConvParams, variant: str) -> bool:
                                                          _variant_code(variant)))
 
 
-def conv_direct_into(x: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, params: ConvParams, variant: str) -> None:
+def conv_direct_into(x: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, params: ConvParams, variant: str,
+                     ws: torch.Tensor | None = None) -> None:
     """tcgen05 convolution that builds the im2win windows in shared memory from the NCHW input."""
     n_img, c_in, h_in, w_in = (int(d) for d in x.shape)
     code = _variant_code(variant)
     lib = _lib.load()
     nbytes = lib.im2win_conv_direct_workspace(c_in, params.c_out, params.h_f, params.w_f, code)
     stream = torch.cuda.current_stream(out.device).cuda_stream
-    ws = _workspace(out.device, stream, nbytes)
+    ws = _workspace(out.device, stream, nbytes) if ws is None else _check_ws(ws, nbytes)
     with torch.cuda.device(out.device):
         rc = lib.im2win_conv_direct(x.data_ptr(), flt.data_ptr(), out.data_ptr(), n_img, c_in, h_in, w_in,
                                     params.c_out, params.h_f, params.w_f, params.stride, params.pad, code,
@@ -440,9 +449,16 @@ class CapturedConv:
         if flt is not None:
             self.filter.copy_(Tensor4(flt).data)
         self.out = torch.empty((n_img, params.c_out, h_out, w_out), dtype=DTYPE, device=dev)
+        # the graph keeps pointing at its workspace: it is owned here, not taken from the shared cache
+        lib = _lib.load()
+        code = _variant_code(variant)
+        ws_bytes = max(lib.im2win_conv_workspace_bytes(c_in, params.c_out, params.h_f, params.w_f, code),
+                       lib.im2win_conv_fused_workspace_bytes(c_in, params.c_out, params.h_f, params.w_f),
+                       lib.im2win_conv_direct_workspace(c_in, params.c_out, params.h_f, params.w_f, code))
+        self._ws = torch.empty(max(ws_bytes, 1 << 16), dtype=torch.uint8, device=dev)
         if variant in ("tf32", "bf16") and direct_preferred(self.input.shape, params, variant):
             def body():
-                conv_direct_into(self.input, self.filter, self.out, params, variant)
+                conv_direct_into(self.input, self.filter, self.out, params, variant, self._ws)
         elif variant in ("tf32", "bf16"):
             dt = torch.bfloat16 if variant == "bf16" else torch.float32
             pad = params.pad
@@ -451,7 +467,7 @@ class CapturedConv:
 
             def body():
                 nhwc_into(self.input, self._mid, pad)
-                conv_fused_into(self._mid, self.filter, self.out, params, variant)
+                conv_fused_into(self._mid, self.filter, self.out, params, variant, self._ws)
         else:
             from .layouts import effective_width, im2win_into
 
@@ -460,7 +476,7 @@ class CapturedConv:
 
             def body():
                 im2win_into(self.input, self._mid, params)
-                conv_windows_into(self._mid, self.filter, self.out, params, w_eff, plan, variant)
+                conv_windows_into(self._mid, self.filter, self.out, params, w_eff, plan, variant, self._ws)
 
         # warm up on a side stream (allocates the workspace, sets kernel attributes), then capture
         side = torch.cuda.Stream(dev)
