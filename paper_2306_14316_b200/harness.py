@@ -19,7 +19,15 @@ import torch
 import torch.nn.functional as F
 
 from .errors import MemoryBudgetError
-from .kernels import basic_windows_into, conv_fused_into, conv_windows_into, nhwc_into, nhwc_pitch
+from .kernels import (
+    basic_windows_into,
+    conv_direct_into,
+    conv_fused_into,
+    conv_windows_into,
+    direct_preferred,
+    nhwc_into,
+    nhwc_pitch,
+)
 from .layouts import im2win_into
 from .plan import TilePlan, gpu_plan
 from .workloads import BENCHMARKS, BenchConfig
@@ -128,6 +136,8 @@ def _stages(cfg: BenchConfig, algorithm: str, x, f, plan: TilePlan | None):
         return tr, cv, out
     if algorithm in ("im2win-tf32", "im2win-bf16"):
         variant = algorithm[7:]
+        if direct_preferred(x.shape, p, variant):  # the library's auto choice: in-SM windows from NCHW
+            return (lambda: None), (lambda: conv_direct_into(x, f, out, p, variant)), out
         xc = torch.empty((cfg.batch, cfg.h_in + 2 * p.pad, cfg.w_in + 2 * p.pad, nhwc_pitch(cfg.c_in, variant)),
                          device=x.device, dtype=torch.bfloat16 if variant == "bf16" else torch.float32)
         return (lambda: nhwc_into(x, xc, p.pad)), (lambda: conv_fused_into(xc, f, out, p, variant)), out
