@@ -121,6 +121,50 @@ __global__ void __launch_bounds__(256) pattern_hint(float* out, int n, int co, i
   }
 }
 
+// Variant: the tile (box_w pixels x co planes) staged in smem, then each plane's run leaves by
+// one TMA bulk store (16-byte aligned middle) + plain stores for the unaligned ends.
+__global__ void __launch_bounds__(256) pattern_bulk(float* out, int n, int co, int ho, int wo, int box_w) {
+  extern __shared__ __align__(128) float stg[];  // [2][co][box_w + 4]
+  const int pitch = (box_w + 4 + 3) / 4 * 4;
+  const int ow_tiles = (wo + box_w - 1) / box_w;
+  const long long tiles = (long long)n * ho * ow_tiles;
+  const long long hw = (long long)ho * wo;
+  int it = 0;
+  for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+    const int owt = t % ow_tiles;
+    const long long rest = t / ow_tiles;
+    const int oh = rest % ho;
+    const long long img = rest / ho;
+    const int ow0 = owt * box_w;
+    const int run = min(box_w, wo - ow0);
+    float* sb = stg + (it & 1) * co * pitch;
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncthreads();
+    const long long base0 = img * co * hw + (long long)oh * wo + ow0;
+    const int head = (4 - (int)(base0 & 3)) & 3;  // same for every plane when hw % 4 == 0
+    for (int i = threadIdx.x; i < co * run; i += blockDim.x) {
+      const int c = i / run, px = i % run;
+      sb[c * pitch + ((head == 0 ? 0 : 4 - head) + px)] = (float)c;  // shift so aligned globals land on aligned smem
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    const int sh = head == 0 ? 0 : 4 - head;
+    const int mid = ((run - head) / 4) * 4;
+    for (int c = threadIdx.x / 32; c < co; c += blockDim.x / 32) {
+      float* dst = out + base0 + (long long)c * hw;
+      const float* src = sb + c * pitch + sh;
+      const int lane = threadIdx.x % 32;
+      if (lane < head) dst[lane] = src[lane];
+      if (lane < run - head - mid) dst[head + mid + lane] = src[head + mid + lane];
+      if (lane == 0 && mid > 0)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + head),
+                     "r"((unsigned)__cvta_generic_to_shared(src + head)), "r"(mid * 4) : "memory");
+    }
+    if (threadIdx.x % 32 == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void fill(float4* out, long long n4) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x)
     out[i] = make_float4(1.f, 2.f, 3.f, 4.f);
@@ -200,6 +244,17 @@ int main() {
     cudaEventRecord(e0); pattern_hint<2><<<148, 256>>>(out, n, co, ho, wo, 111); cudaEventRecord(e1);
     cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
     printf("pattern evict_last: %.3f ms  %.2f TB/s\n", ms, elems * 4 / (ms * 1e-3) / 1e12);
+  }
+  {
+    float ms;
+    for (int bw : {111, 222}) {
+      const size_t sm = 2ull * co * ((bw + 7) / 4 * 4) * 4;
+      cudaFuncSetAttribute(pattern_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      pattern_bulk<<<148, 256, sm>>>(out, n, co, ho, wo, bw);
+      cudaEventRecord(e0); pattern_bulk<<<148, 256, sm>>>(out, n, co, ho, wo, bw); cudaEventRecord(e1);
+      cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+      printf("bulk box_w=%d: %.3f ms  %.2f TB/s  (%s)\n", bw, ms, elems * 4 / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+    }
   }
   fill<<<148 * 8, 256>>>((float4*)out, elems / 4);
   cudaEventRecord(e0);
