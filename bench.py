@@ -391,6 +391,64 @@ def main() -> None:
                "note": "transform + FFMA conv (ascending k, one rounding per multiply-add); bounded by the FFMA peak"}
         del fma_out
 
+    # ---- the other BASELINE.json configs on this GPU (rank 0): config 1 (pad 1, native
+    # padding) and config 3 (conv1 at N=256, the window-transform stress case) ----
+    other_cfgs = None
+    if rank == 0:
+        from paper_2306_14316_b200.workloads import BENCHMARKS as _B
+
+        def timed_pair(fn_tr, fn_cv, reps=5):
+            fn_tr()
+            fn_cv()
+            torch.cuda.synchronize(dev)
+            bt = bc = 1e30
+            for _ in range(reps):
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                e[0].record(stream)
+                fn_tr()
+                e[1].record(stream)
+                fn_cv()
+                e[2].record(stream)
+                torch.cuda.synchronize(dev)
+                bt, bc = min(bt, e[0].elapsed_time(e[1])), min(bc, e[1].elapsed_time(e[2]))
+            return bt, bc
+
+        other_cfgs = {}
+        # config 1: N=8 C=64 56x56 K=64 3x3 s1 pad 1 -> padding inside the transform
+        g1 = torch.Generator(device=dev).manual_seed(0)
+        p1 = pkg.ConvParams(64, 64, 3, 3, 1, pad=1)
+        x1 = torch.randn((8, 64, 56, 56), device=dev, generator=g1)
+        f1 = torch.randn((64, 64, 3, 3), device=dev, generator=g1)
+        w1 = torch.empty((8, 64, 56, 3 * 58), device=dev)
+        o1 = torch.empty((8, 64, 56, 56), device=dev)
+        t_tr, t_cv = timed_pair(lambda: im2win_into(x1, w1, p1),
+                                lambda: conv_windows_into(w1, f1, o1, p1, 58, None, args.variant))
+        fl1 = 2 * 8 * 64 * 56 * 56 * 64 * 9
+        other_cfgs["config1_n8_pad1"] = {"tflops": fl1 / ((t_tr + t_cv) * 1e-3) / 1e12,
+                                         "tflops_conv_only": fl1 / (t_cv * 1e-3) / 1e12,
+                                         "transform_ms": t_tr, "conv_ms": t_cv,
+                                         "note": "zero padding inside the transform (ConvParams.pad=1); the "
+                                                 "golden checksum of this config is a GPU test"}
+        del x1, f1, w1, o1
+        # config 3: conv1 (3x227x227, 96x11x11, s4) at N=256
+        c3 = replace(_B["conv1"], batch=256, seed=3)
+        g3 = torch.Generator(device=dev).manual_seed(3)
+        h3, w3o = c3.out_dims
+        x3 = torch.randn((256, 3, 227, 227), device=dev, generator=g3)
+        f3 = torch.randn((96, 3, 11, 11), device=dev, generator=g3)
+        wn3 = torch.empty((256, 3, h3, 11 * c3.w_eff), device=dev)
+        o3 = torch.empty((256, 96, h3, w3o), device=dev)
+        t_tr, t_cv = timed_pair(lambda: im2win_into(x3, wn3, c3.params),
+                                lambda: conv_windows_into(wn3, f3, o3, c3.params, c3.w_eff, None, args.variant))
+        other_cfgs["config3_conv1_n256"] = {"tflops": c3.flops / ((t_tr + t_cv) * 1e-3) / 1e12,
+                                            "tflops_conv_only": c3.flops / (t_cv * 1e-3) / 1e12,
+                                            "transform_ms": t_tr, "conv_ms": t_cv,
+                                            "transform_gbs": c3.transform_bytes() / (t_tr * 1e-3) / 1e9,
+                                            "transform_frac_of_hbm": c3.transform_bytes() / (t_tr * 1e-3) / 1e9
+                                            / peaks["hbm_gbs"]}
+        del x3, f3, wn3, o3
+        torch.cuda.empty_cache()
+
     # ---- FP32 CUDA-core peak probe (roofline denominator) ----
     lib = _lib.load()
     sink = torch.empty(256, device=dev)
@@ -674,6 +732,7 @@ def main() -> None:
         "layers": per_layer,
         "baselines": baselines,
         "fp32_fma_variant": fma,
+        "other_configs": other_cfgs,
         "tensor_core_variants": tc,
         "peaks": {"fp32_exact_tflops": peak["exact"], "fp32_ffma_tflops": peak["ffma"],
                   "hbm_gbs": peaks["hbm_gbs"], "source": peaks["source"]},
