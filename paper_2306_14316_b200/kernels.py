@@ -341,9 +341,23 @@ class HostConv:
             _lib.load().im2win_conv_host_wait(self._ticket)
 
 
+class _MultiHostConv:
+    """Handles of one host convolution split across several GPUs (batch slices)."""
+
+    def __init__(self, out, parts):
+        self.out = out
+        self._parts = parts
+
+    def wait(self) -> torch.Tensor:
+        for h in self._parts:
+            h.wait()
+        self._parts = []
+        return self.out
+
+
 def conv_im2win_opt_host(inp, flt, params: ConvParams, plan: TilePlan | None = None, *,
                          variant: str = "fp32-exact", out: torch.Tensor | None = None, chunk_images: int = 0,
-                         device=None, wait: bool = True):
+                         device=None, devices=None, wait: bool = True):
     """`conv_im2win_opt` for host operands, as the reference is called (optimized.py:237-241).
 
     Host input and filter in, host output back (a CPU float32 tensor; pass a
@@ -353,7 +367,27 @@ def conv_im2win_opt_host(inp, flt, params: ConvParams, plan: TilePlan | None = N
     operands let the copies overlap; pageable ones work but serialise.
     With wait=False the call returns a `HostConv` at once; consecutive
     submissions overlap each other (uploads of one with downloads of the last).
+    `devices` (a list of CUDA devices) splits the batch into contiguous slices, one
+    per device, each streamed over its own PCIe link from one process (images are
+    independent, reference.py:78-90, so the result is bit-identical to one device).
     """
+    if devices is not None and len(devices) > 1:
+        from .sharding import shard_bounds
+
+        x = _host_f32(inp, 4)
+        f = _host_f32(flt, 4)
+        n_img = int(x.shape[0])
+        if out is None:
+            h_out, w_out = output_dims(int(x.shape[2]), int(x.shape[3]), params)
+            out = torch.empty((n_img, params.c_out, h_out, w_out), dtype=DTYPE, pin_memory=True)
+        parts = []
+        for r, d in enumerate(devices):
+            lo, hi = shard_bounds(n_img, len(devices), r)
+            if hi > lo:
+                parts.append(conv_im2win_opt_host(x[lo:hi], f, params, plan, variant=variant, out=out[lo:hi],
+                                                  chunk_images=chunk_images, device=d, wait=False))
+        handle = _MultiHostConv(out, parts)
+        return handle.wait() if wait else handle
     x = _host_f32(inp, 4)
     f = _host_f32(flt, 4)
     n_img, c_in, h_in, w_in = (int(d) for d in x.shape)
@@ -392,7 +426,7 @@ def conv_im2win_opt_host(inp, flt, params: ConvParams, plan: TilePlan | None = N
 
 
 def conv_im2win_opt_host_batch(jobs, *, variant: str = "fp32-exact", outs=None, chunk_images: int = 0,
-                               device=None) -> list:
+                               device=None, devices=None) -> list:
     """Several independent host-operand convolutions (e.g. the layers of a benchmark step).
 
     `jobs` is a list of (inp, flt, params); `outs` optional page-locked outputs in the same
@@ -415,7 +449,8 @@ def conv_im2win_opt_host_batch(jobs, *, variant: str = "fp32-exact", outs=None, 
     for i in order:
         inp, flt, params = jobs[i]
         handles[i] = conv_im2win_opt_host(inp, flt, params, variant=variant, chunk_images=chunk_images,
-                                          out=None if outs is None else outs[i], device=device, wait=False)
+                                          out=None if outs is None else outs[i], device=device, devices=devices,
+                                          wait=False)
     return [h.wait() for h in handles]
 
 

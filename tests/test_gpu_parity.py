@@ -498,3 +498,17 @@ def test_tc_direct_geometries(variant):
         else:
             out = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path="direct").numpy()
         assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (n, c, h, w, co, hf, wf, s, p)
+
+
+def test_host_pipeline_device_list_slices():
+    """devices=[...] splits the batch into per-device slices submitted concurrently; with the one
+    GPU of this box listed several times the slices share it and the result is still the
+    single-call result bit for bit (ragged slices included)."""
+    cfg = replace(BENCHMARKS["conv9"], batch=7, seed=12)
+    inp, flt = make_inputs(cfg)
+    ref = pkg.conv_im2win_opt_host(inp, flt, cfg.params).numpy()
+    for devs in ([0, 0], [0, 0, 0], ["cuda:0"] * 4):
+        got = pkg.conv_im2win_opt_host(inp, flt, cfg.params, devices=devs, chunk_images=1).numpy()
+        assert bits_equal(got, ref), devs
+    outs = pkg.conv_im2win_opt_host_batch([(inp, flt, cfg.params)], devices=[0, 0])
+    assert bits_equal(outs[0].numpy(), ref)
