@@ -4,7 +4,12 @@ Public names follow the reference package (/root/reference/pkg/src/winconv/__ini
 for the hot path: `im2win`, `Im2winTensor`, `conv_im2win_opt`,
 `compute_from_windows_opt`, `TilePlan`, `default_plan`, `GemmDims`,
 `ConvParams`, `Tensor4`, `output_dims`, `max_rel_diff`, `footprint_elems`,
-`im2win_gather` and the error types.  Operands live on CUDA devices; the
+`im2win_gather`, the error types and the benchmark harness (`run_bench`,
+`run_ablation`, `report_csv`, `footprint_report`, `BenchRecord`, `ALGORITHMS`).
+The reference's CPU baselines (`conv_direct`, `conv_im2col_gemm`,
+`conv_implicit_gemm`, `gemm`, `im2col`, `Mat2`) and its worker pool are not
+rebuilt: on the GPU the baselines are cuDNN and im2col+cuBLAS (harness
+algorithms "cudnn" / "im2col-cublas") and the CPU oracle lives in oracle/.  Operands live on CUDA devices; the
 kernels are hand-written sm_100a CUDA in libim2win_sm100.so (csrc/), reached
 through a C ABI (include/im2win_sm100.h).  There is no CPU fallback.
 """
@@ -32,12 +37,19 @@ from .kernels import (
 )
 from .workloads import BENCHMARKS, BenchConfig, make_inputs
 from .fixture_io import read_tensor, write_tensor
+from .harness import ALGORITHMS, BenchRecord, footprint_report, report_csv, run_ablation, run_bench
 
 __version__ = "0.1.0"
 
 VARIANTS = ("fp32-exact", "fp32-fma", "tf32", "bf16")
 
 __all__ = [
+    "ALGORITHMS",
+    "BenchRecord",
+    "footprint_report",
+    "report_csv",
+    "run_ablation",
+    "run_bench",
     "BENCHMARKS",
     "BenchConfig",
     "CapturedConv",
