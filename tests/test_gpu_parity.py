@@ -512,3 +512,12 @@ def test_host_pipeline_device_list_slices():
         assert bits_equal(got, ref), devs
     outs = pkg.conv_im2win_opt_host_batch([(inp, flt, cfg.params)], devices=[0, 0])
     assert bits_equal(outs[0].numpy(), ref)
+
+
+def test_memory_budget_refusal():
+    """run_bench refuses a configuration that cannot fit before allocating anything
+    (reference bench.py:179-183, test_bench.py:114-120), with the byte counts."""
+    cfg = replace(BENCHMARKS["conv4"], batch=100_000)
+    with pytest.raises(pkg.MemoryBudgetError) as e:
+        pkg.run_bench(cfg, "im2win-opt", repeats=1)
+    assert e.value.required_bytes > e.value.available_bytes > 0

@@ -153,3 +153,27 @@ def test_output_dims_with_padding():
     with pytest.raises(pkg.GeometryError):
         pkg.output_dims(1, 1, pkg.ConvParams(1, 1, 5, 5, 1, pad=1))
     assert pkg.ConvParams(1, 1, 3, 3) == pkg.ConvParams(1, 1, 3, 3, 1, 0)
+
+
+def test_footprint_report_dominance():
+    """Reference acceptance criterion: the window layout is smaller than im2col on every layer
+    (test_acceptance.py:84-103); the report carries the same counts as footprint_elems."""
+    from dataclasses import replace
+
+    rows = pkg.footprint_report([replace(c, batch=1) for c in pkg.BENCHMARKS.values()])
+    assert [r.name for r in rows] == list(pkg.BENCHMARKS)
+    for r, cfg in zip(rows, pkg.BENCHMARKS.values()):
+        assert r.raw_elems < r.im2win_elems < r.im2col_elems
+        assert r.im2win_elems == pkg.footprint_elems("im2win", 1, cfg.c_in, cfg.h_in, cfg.w_in, cfg.params)
+        assert 0 < r.reduction_pct < 100
+    assert rows[0].im2win_elems == 412_005
+
+
+def test_harness_names_match_reference():
+    assert pkg.ALGORITHMS[0] == "im2win-opt" and "cudnn" in pkg.ALGORITHMS
+    from paper_2306_14316_b200 import harness
+
+    assert harness.ABLATION_VARIANTS == ("full", "-prefetch-double-buffer", "-vectorized-load", "-micro-kernel")
+    assert harness.CSV_COLUMNS[:17] == ("name", "algorithm", "variant", "batch", "repeats", "h_o", "w_o", "flops",
+                                        "transform_s", "compute_s", "total_s", "tflops", "raw_elems",
+                                        "im2col_elems", "im2win_elems", "footprint_reduction_pct", "checksum")
