@@ -46,10 +46,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
                     "-I", str(PKG.parent / "include")]
     if verbose:
         flags += ["-Xptxas", "-v"]
-    for src in SOURCES:
+    def compile_one(src):
         obj = build_dir / (Path(src).stem + ".o")
         cmd = [nvcc()] + flags + ["-c", str(CSRC / src), "-o", str(obj)]
-        res = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    # the translation units are independent: compile them in parallel
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as pool:
+        results = list(pool.map(compile_one, SOURCES))
+    for src, obj, res in results:
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
         if verbose and res.stderr:
