@@ -396,6 +396,10 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
   const int BM = kBM[cfg], BK = kBKc[cfg];
   const int Mp = static_cast<int>((c_out + BM - 1) / BM * BM);
   const int Kp = static_cast<int>((K + BK - 1) / BK * BK);
+  if ((reinterpret_cast<uintptr_t>(workspace) & 15u) != 0) {
+    *err = "im2win_conv_f32: workspace must be 16-byte aligned";
+    return 1;
+  }
   float* fltT = static_cast<float*>(workspace);
   int* delta = reinterpret_cast<int*>(fltT + static_cast<int64_t>(Kp) * Mp);
 
@@ -419,7 +423,7 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
   a.hw = static_cast<uint32_t>(hw);
   a.fd_hw = FastDiv(static_cast<uint32_t>(hw));
   a.fd_wo = FastDiv(static_cast<uint32_t>(w_out));
-  a.vec_out = (hw % 4 == 0) ? 1u : 0u;
+  a.vec_out = (hw % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0) ? 1u : 0u;
 
   cudaError_t e = cudaSuccess;
 #ifndef IM2WIN_SIMT_STAGES

@@ -397,6 +397,10 @@ int im2win_launch_transform_cl(const float* src, void* dst, int64_t n, int64_t c
     *err = "im2win_transform_cl: c must be a multiple of 4";
     return 1;
   }
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) != 0 || (reinterpret_cast<uintptr_t>(src) & 3) != 0) {
+    *err = "im2win_transform_cl: dst must be 16-byte aligned and src 4-byte aligned";
+    return 1;
+  }
   if (total >= (1ll << 32) || n * c * h * w >= (1ll << 40)) {
     *err = "im2win_transform_cl: extents exceed the kernel's index range";
     return 1;

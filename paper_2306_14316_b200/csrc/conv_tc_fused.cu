@@ -456,6 +456,10 @@ int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c
     *err = "nchw_to_nhwc: extents exceed the kernel's index range";
     return 1;
   }
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) != 0 || (reinterpret_cast<uintptr_t>(src) & 3) != 0) {
+    *err = "nchw_to_nhwc: dst must be 16-byte aligned and src 4-byte aligned";
+    return 1;
+  }
   PadMap pm;
   pm.pad = static_cast<uint32_t>(pad);
   pm.wp = static_cast<uint32_t>(wp);

@@ -27,6 +27,7 @@ struct TransformArgs {
   uint32_t rows_per_cta;
   FastDiv fd_ho, fd_rl, fd_hf, fd_weff;
   uint32_t pad;         // zero padding on every side (pipelined kernel only); h_out/w_eff are padded geometry
+  uint32_t src_mis, dst_mis;  // (ptr % 16) / 4 of src / dst: the staged kernel aligns its float4s to the address
 };
 
 IM2WIN_DEVICE uint64_t in_row_of(const TransformArgs& a, uint32_t g) {
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(256) im2win_transform_kernel(const TransformAr
   const uint64_t f_begin = r_lo * a.w_in;
   const uint32_t f_count = static_cast<uint32_t>((r_hi - r_lo) * a.w_in);
   const float* src = a.src + f_begin;
-  const uint32_t f_head = min(f_count, static_cast<uint32_t>((4u - (f_begin & 3u)) & 3u));
+  const uint32_t f_head = min(f_count, static_cast<uint32_t>((4u - ((f_begin + a.src_mis) & 3u)) & 3u));
   const uint32_t tshift = (4u - f_head) & 3u;
   {
     const uint32_t nvec = (f_count - f_head) >> 2;
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(256) im2win_transform_kernel(const TransformAr
   // columns: reads hit consecutive banks, writes stride Hf (odd -> conflict free).
   const uint64_t e_begin = static_cast<uint64_t>(g0) * a.row_len;
   const uint32_t count = nrows_out * a.row_len;
-  const uint32_t head = min(count, static_cast<uint32_t>((4u - (e_begin & 3u)) & 3u));
+  const uint32_t head = min(count, static_cast<uint32_t>((4u - ((e_begin + a.dst_mis) & 3u)) & 3u));
   const uint32_t oshift = (4u - head) & 3u;
   __syncthreads();
   {
@@ -419,6 +420,12 @@ int im2win_launch_transform(const float* src, float* dst, int64_t n, int64_t c, 
   a.fd_hf = FastDiv(a.h_f);
   a.fd_weff = FastDiv(a.w_eff);
   a.pad = static_cast<uint32_t>(pad);
+  a.src_mis = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(src) & 15u) >> 2);
+  a.dst_mis = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(dst) & 15u) >> 2);
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 3u) != 0) {
+    *err = "im2win_transform_f32: buffers must be 4-byte aligned";
+    return 1;
+  }
   (void)w_f;
   const bool aligned = (reinterpret_cast<uintptr_t>(src) & 15u) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
   // pipelined path: two stages of (row offsets, staged input, output chunk)

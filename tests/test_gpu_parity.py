@@ -521,3 +521,29 @@ def test_memory_budget_refusal():
     with pytest.raises(pkg.MemoryBudgetError) as e:
         pkg.run_bench(cfg, "im2win-opt", repeats=1)
     assert e.value.required_bytes > e.value.available_bytes > 0
+
+
+@pytest.mark.parametrize("pad", [0, 2])
+def test_unaligned_and_degenerate_inputs(pad):
+    """Operands at a 4-byte offset (the transform's 16-byte TMA path cannot take them: the
+    legacy kernel / an aligned copy is used), one-pixel outputs (filter = padded input) and a
+    single image all give the oracle's bits."""
+    rng = np.random.default_rng(77 + pad)
+    base = torch.from_numpy(rng.standard_normal(1 + 2 * 4 * 9 * 11, dtype=np.float32)).to(DEV)
+    x = base[1:].view(2, 4, 9, 11)  # data_ptr % 16 == 4
+    assert x.data_ptr() % 16 != 0
+    flt = rng.standard_normal((5, 4, 3, 3), dtype=np.float32)
+    params = pkg.ConvParams(4, 5, 3, 3, 2, pad=pad)
+    xn = x.cpu().numpy()
+    win = pkg.im2win(x, params)
+    assert bits_equal(win.data.cpu().numpy(), orc.im2win_fill(_pad_np(xn, pad), 3, 3, 2))
+    out = pkg.conv_im2win_opt(x, torch.from_numpy(flt).to(DEV), params)
+    assert bits_equal_nan_as_class(out.numpy(), orc.conv_direct(_pad_np(xn, pad), flt, 2))
+    # filter as large as the (padded) input: one output pixel per image and channel
+    h = 7 - 2 * pad
+    xi = rng.standard_normal((1, 3, h, h), dtype=np.float32)
+    fi = rng.standard_normal((2, 3, 7, 7), dtype=np.float32)
+    p1 = pkg.ConvParams(3, 2, 7, 7, 1, pad=pad)
+    o1 = pkg.conv_im2win_opt(xi, fi, p1)
+    assert o1.dims == (1, 2, 1, 1)
+    assert bits_equal_nan_as_class(o1.numpy(), orc.conv_direct(_pad_np(xi, pad), fi, 1))
