@@ -28,6 +28,12 @@
 #ifndef IM2WIN_SIMT_BRANCHLESS
 #define IM2WIN_SIMT_BRANCHLESS 1  // measured +0.7% on the 12-layer step (fewer branch/convergence ops)
 #endif
+#ifndef IM2WIN_SIMT_NOCLAMP
+#define IM2WIN_SIMT_NOCLAMP 0  // padded k: ignore-src predicate only, no address clamp
+#endif
+#ifndef IM2WIN_SIMT_PART_ROWS
+#define IM2WIN_SIMT_PART_ROWS 4  // window rows gathered per interleaved hook
+#endif
 #ifndef IM2WIN_SIMT_INTERLEAVE
 #define IM2WIN_SIMT_INTERLEAVE 1
 #endif
@@ -97,8 +103,9 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? 2 : ((BM / MT
   constexpr int TXN = BN / MT;                // threads along n
   constexpr int CPT = (BN + NT - 1) / NT;     // gather columns per thread
   constexpr int HALVES = MT / 4;              // 4-wide quadrants per axis
-  constexpr int PARTS = BK / 4;               // gather parts per slab
-  static_assert(BK % 4 == 0, "BK must be a multiple of 4 (int4 delta loads)");
+  constexpr int PR = IM2WIN_SIMT_PART_ROWS;   // window rows per gather part
+  constexpr int PARTS = BK / PR;              // gather parts per slab
+  static_assert(PR % 4 == 0 && BK % PR == 0, "parts are whole int4 delta loads");
   static_assert(MT == 4 || MT == 8, "micro-tile is 4x4 or 8x8");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* As = reinterpret_cast<float*>(smem_raw);  // [STAGES][BK][BM]
@@ -153,10 +160,14 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? 2 : ((BM / MT
   };
   // window slab rows [4*part, 4*part+4): each gathering thread owns whole columns
   auto load_window_part = [&](int kt, int slot, int part) {
-    const int4 v = SD ? *reinterpret_cast<const int4*>(dtab + kt * BK + 4 * part)
-                      : __ldg(reinterpret_cast<const int4*>(dtab + kt * BK + 4 * part));
-    const int d[4] = {v.x, v.y, v.z, v.w};
-    float* bdst = Bs + slot * BK * BN + 4 * part * BN;
+    int d[PR];
+#pragma unroll
+    for (int q = 0; q < PR / 4; ++q) {
+      const int4 v = SD ? *reinterpret_cast<const int4*>(dtab + kt * BK + PR * part + 4 * q)
+                        : __ldg(reinterpret_cast<const int4*>(dtab + kt * BK + PR * part + 4 * q));
+      d[4 * q] = v.x; d[4 * q + 1] = v.y; d[4 * q + 2] = v.z; d[4 * q + 3] = v.w;
+    }
+    float* bdst = Bs + slot * BK * BN + PR * part * BN;
     const bool full = kt < k_full;
 #if IM2WIN_SIMT_BRANCHLESS
     // branch-free form: every element predicated (padded k -> delta -1 -> zero fill)
@@ -165,9 +176,14 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? 2 : ((BM / MT
       const int c = tid + j * NT;
       if (CPT * NT == BN || c < BN) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
+        for (int kk = 0; kk < PR; ++kk) {
           const bool ok = d[kk] >= 0;
+#if IM2WIN_SIMT_NOCLAMP
+          // ignore-src copies never touch the source: the address need not be valid
+          cp_async_4_zfill(smem_u32(bdst + kk * BN + c), bsrc[j] + d[kk], bzero[j] || !ok);
+#else
           cp_async_4_zfill(smem_u32(bdst + kk * BN + c), bsrc[j] + (ok ? d[kk] : 0), bzero[j] || !ok);
+#endif
         }
       }
     }
@@ -180,10 +196,10 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? 2 : ((BM / MT
       if (c < BN) {
         if (full) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) cp_async_4_zfill(smem_u32(bdst + kk * BN + c), bsrc[j] + d[kk], bzero[j]);
+          for (int kk = 0; kk < PR; ++kk) cp_async_4_zfill(smem_u32(bdst + kk * BN + c), bsrc[j] + d[kk], bzero[j]);
         } else {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
+          for (int kk = 0; kk < PR; ++kk) {
             const bool ok = d[kk] >= 0;
             cp_async_4_zfill(smem_u32(bdst + kk * BN + c), ok ? bsrc[j] + d[kk] : a.win, bzero[j] || !ok);
           }
@@ -212,7 +228,7 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? 2 : ((BM / MT
     const float* bs = Bs + slot * BK * BN;
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      if (kk % 4 == 0) hook(kk / 4);
+      if (kk % PR == 0) hook(kk / PR);
       float fa[MT], fb[MT];
       if constexpr (VEC) {
 #pragma unroll

@@ -31,5 +31,13 @@ for (n, c, h, w, co, hf, wf, s, p) in cases:
                 continue
             pkg.conv_im2win_opt(x, f, params, variant=v, tc_path=path)
     pkg.conv_im2win_opt_host(x.cpu(), f.cpu(), params, chunk_images=1)
+# 4-byte-offset operands (the staged transform aligns its 16-byte copies to the address)
+for (n, c, h, w, co, hf, wf, s, p) in cases[:3]:
+    base = torch.from_numpy(rng.standard_normal(1 + n * c * h * w, dtype=np.float32)).cuda()
+    x = base[1:].view(n, c, h, w)
+    f = torch.from_numpy(rng.standard_normal((co, c, hf, wf), dtype=np.float32)).cuda()
+    params = pkg.ConvParams(c, co, hf, wf, s, pad=p)
+    pkg.conv_im2win_opt(x, f, params)
+    pkg.im2win(x, params)
 torch.cuda.synchronize()
 print("sanitize cases done")
