@@ -28,6 +28,7 @@ constexpr int kDirThreads = 16 * 32;
 constexpr int kProducers = 256;
 constexpr int kProdWarps = kProducers / 32;
 constexpr int kDirEpiWarps = 4;
+constexpr int kDirColIters = 16;  // patch rows up to 512 floats (checked by plan_direct)
 
 struct DirectArgs {
   const float* __restrict__ x;   // NCHW input
@@ -146,28 +147,51 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
     // pixel (r_row, r_col) reads patch rows r_row*s + fh, columns r_col*s + fw = phase fw%s, index r_col + fw/s
     const uint32_t pix_base = (r_row * a.stride) * a.prow_pitch + r_col;
     const uint32_t prows_total = a.c_in * a.prow;
-    // patch of tile t -> buffer at smem address `pb`: 4-byte cp.async, zero-filled outside the image,
-    // columns phase-major (column s*q + ph stored at ph*pcolq + q) so lanes later read consecutive words
+    // Patch columns are read in natural order (lane = column: coalesced) and stored phase-major
+    // (column s*q + ph at ph*pcolq + q) so lanes later read consecutive words.  The smem offset
+    // of column lane + 32*i is the same for every row of every tile: computed once.
+    uint32_t col_dst[kDirColIters];
+    uint32_t col_live = 0;  // bit i: column lane + 32*i lies inside the patch row
+#pragma unroll
+    for (int i = 0; i < kDirColIters; ++i) {
+      const uint32_t col = lane + 32 * i;
+      col_dst[i] = 4 * ((col % a.stride) * a.pcolq + col / a.stride);
+      if (col < a.prow_pitch) col_live |= 1u << i;
+    }
+    // patch of tile t -> buffer at smem address `pb`: 4-byte cp.async, zero-filled outside the image
     auto issue_patch = [&](uint32_t t, uint32_t pb) {
       const uint32_t owt = t % a.ow_tiles;
       const uint32_t rest = t / a.ow_tiles;
       const uint32_t oh0 = (rest % a.oh_tiles) * a.rows;
       const uint32_t img = rest / a.oh_tiles;
-      const int64_t ih0 = static_cast<int64_t>(oh0) * a.stride - a.pad;
-      const int64_t iw0 = static_cast<int64_t>(owt * a.box_w) * a.stride - a.pad;
+      const int ih0 = static_cast<int>(oh0 * a.stride) - static_cast<int>(a.pad);
+      const int iw0 = static_cast<int>(owt * a.box_w * a.stride) - static_cast<int>(a.pad);
       const float* xi = a.x + static_cast<int64_t>(img) * a.c_in * a.h_in * a.w_in;
+      uint32_t col_in = 0;  // bit i: column lane + 32*i is inside the image (this tile)
+#pragma unroll
+      for (int i = 0; i < kDirColIters; ++i) {
+        const int iw = iw0 + static_cast<int>(lane + 32 * i);
+        if (iw >= 0 && iw < static_cast<int>(a.w_in)) col_in |= 1u << i;
+      }
+      col_in &= col_live;
+      uint32_t c = warp / a.prow, rr = warp % a.prow;
       for (uint32_t pr = warp; pr < prows_total; pr += kProdWarps) {
-        const uint32_t c = pr / a.prow, rr = pr % a.prow;
-        const int64_t ih = ih0 + rr;
-        const bool in_row = ih >= 0 && ih < a.h_in;
-        const float* src = xi + (static_cast<int64_t>(c) * a.h_in + (in_row ? ih : 0)) * a.w_in;
+        const int ih = ih0 + static_cast<int>(rr);
+        const bool in_row = ih >= 0 && ih < static_cast<int>(a.h_in);
+        const uint32_t m = in_row ? col_in : 0u;
+        const float* src = xi + (static_cast<int64_t>(c) * a.h_in + (in_row ? ih : 0)) * a.w_in + iw0 + lane;
         const uint32_t dst_row = pb + pr * a.prow_pitch * 4;
-        for (uint32_t ph = 0; ph < a.stride; ++ph) {
-          for (uint32_t q = lane; q < a.pcolq; q += 32) {
-            const int64_t iw = iw0 + static_cast<int64_t>(q) * a.stride + ph;
-            const bool ok = in_row && iw >= 0 && iw < a.w_in;
-            cp_async_4_zfill(dst_row + 4 * (ph * a.pcolq + q), ok ? src + iw : xi, !ok);
+#pragma unroll
+        for (int i = 0; i < kDirColIters; ++i) {
+          if ((col_live >> i) & 1u) {
+            const bool ok = (m >> i) & 1u;
+            cp_async_4_zfill(dst_row + col_dst[i], ok ? src + 32 * i : xi, !ok);
           }
+        }
+        rr += kProdWarps;
+        while (rr >= a.prow) {
+          rr -= a.prow;
+          ++c;
         }
       }
       cp_async_commit();
@@ -378,6 +402,7 @@ bool plan_direct(int64_t n, int64_t c_in, int64_t h, int64_t w, int64_t c_out, i
   a.pcol = (a.box_w - 1) * a.stride + a.w_f;
   a.pcolq = (a.pcol + a.stride - 1) / a.stride;
   a.prow_pitch = a.stride * a.pcolq;
+  if (a.prow_pitch > 32u * kDirColIters) return false;
   // shared memory: A ring + resident filter + patch buffers
   const size_t b_bytes = static_cast<size_t>(slabs) * p.N * kRowBytes;
   const size_t patch_bytes = static_cast<size_t>(c_in) * a.prow * a.prow_pitch * 4;

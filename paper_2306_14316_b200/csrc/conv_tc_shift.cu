@@ -333,7 +333,11 @@ int im2win_try_conv_tc_shift(const void* x_cl, const float* flt, float* out, voi
   using namespace im2win::tc;
   if (stride != 1 || (w_f != 3 && w_f != 5)) return 0;
   const char* env = getenv("IM2WIN_SHIFT");
-  if (env && atoi(env) == 0) return 0;
+  const int mode = env ? atoi(env) : 1;  // 0 off, 1 auto, 2 wherever legal
+  if (mode == 0) return 0;
+  // few channels (conv7, C = 3): a tap's A row is mostly channel padding; measured slower than
+  // the generic kernel (tools/tc_kernels.py conv7: 28 vs 33 TF)
+  if (mode == 1 && c_in < 16) return 0;
   const int64_t h_out = h - h_f + 1, w_out = w - w_f + 1;
   ShiftArgs a{};
   a.out = out;

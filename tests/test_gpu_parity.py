@@ -327,7 +327,7 @@ def test_host_pipeline_nonblocking_overlapped_submissions():
 def test_tc_kernel_selections_all_layers(select, variant, layer_goldens, monkeypatch):
     """Each fused tensor-core kernel (phase-shift / window-shift / generic TMA window) is
     within tolerance on every layer where it applies (forced through the library's env switches)."""
-    env = {"phase": ("2", "0"), "shift": ("0", "1"), "generic": ("0", "0")}[select]
+    env = {"phase": ("2", "0"), "shift": ("0", "2"), "generic": ("0", "0")}[select]
     monkeypatch.setenv("IM2WIN_PHASE", env[0])
     monkeypatch.setenv("IM2WIN_SHIFT", env[1])
     for name in BENCHMARKS:

@@ -24,7 +24,7 @@ from paper_2306_14316_b200.kernels import (  # noqa: E402
 layers = sys.argv[1].split(",") if len(sys.argv) > 1 and sys.argv[1] != "all" else list(pkg.BENCHMARKS)
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 dev = torch.device("cuda:0")
-SELECT = {"phase": {"IM2WIN_PHASE": "2", "IM2WIN_SHIFT": "0"}, "shift": {"IM2WIN_PHASE": "0", "IM2WIN_SHIFT": "1"},
+SELECT = {"phase": {"IM2WIN_PHASE": "2", "IM2WIN_SHIFT": "0"}, "shift": {"IM2WIN_PHASE": "0", "IM2WIN_SHIFT": "2"},
           "generic": {"IM2WIN_PHASE": "0", "IM2WIN_SHIFT": "0"}, "auto": {"IM2WIN_PHASE": "1", "IM2WIN_SHIFT": "1"}}
 
 
