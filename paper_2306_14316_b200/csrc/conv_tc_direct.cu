@@ -18,6 +18,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "tc_common.cuh"
 
@@ -29,6 +30,9 @@ constexpr int kProducers = 256;
 constexpr int kProdWarps = kProducers / 32;
 constexpr int kDirEpiWarps = 4;
 constexpr int kDirColIters = 16;  // patch rows up to 512 floats (checked by plan_direct)
+#ifndef IM2WIN_DIRECT_SPLIT_BUILD
+#define IM2WIN_DIRECT_SPLIT_BUILD 1  // padded-k check only in the last slab
+#endif
 
 struct DirectArgs {
   const float* __restrict__ x;   // NCHW input
@@ -145,7 +149,8 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
     const uint32_t r_row = arow_i / a.box_w, r_col = arow_i % a.box_w;  // this thread's pixel inside the tile
     const bool row_ok = arow_i < a.rows * a.box_w;
     // pixel (r_row, r_col) reads patch rows r_row*s + fh, columns r_col*s + fw = phase fw%s, index r_col + fw/s
-    const uint32_t pix_base = (r_row * a.stride) * a.prow_pitch + r_col;
+    // rows past the tile's pixels build from pixel 0 (in-bounds reads; the epilogue drops them)
+    const uint32_t pix_base = row_ok ? (r_row * a.stride) * a.prow_pitch + r_col : 0u;
     const uint32_t prows_total = a.c_in * a.prow;
     // Patch columns are read in natural order (lane = column: coalesced) and stored phase-major
     // (column s*q + ph at ph*pcolq + q) so lanes later read consecutive words.  The smem offset
@@ -220,8 +225,9 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
         else cp_async_commit();
       }
       const uint32_t my_base = pb + 4 * pix_base;
-      for (uint32_t sl = 0; sl < a.slabs; ++sl) {
-        mbar_wait(&a_empty[stage], phase ^ 1);
+      // one slab: this thread's four 16-byte chunks of its A row; only the last slab holds
+      // padded k (offset -1 -> zero), so the others skip the check
+      auto build_slab = [&](uint32_t sl, auto check) {
         const uint32_t arow = smem_u32(a_ring + stage * kATile) + arow_i * kRowBytes;
         const uint32_t ko = koff_s + 4 * sl * kBK;
 #pragma unroll
@@ -237,12 +243,24 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
           }
           float v[kPerChunk];
 #pragma unroll
-          for (int e = 0; e < kPerChunk; ++e) v[e] = (row_ok && off[e] >= 0) ? lds32(my_base + 4 * off[e]) : 0.0f;
+          for (int e = 0; e < kPerChunk; ++e) {
+            if constexpr (decltype(check)::value) v[e] = off[e] >= 0 ? lds32(my_base + 4 * off[e]) : 0.0f;
+            else v[e] = lds32(my_base + 4 * off[e]);
+          }
           uint32_t w[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) w[q] = BF16 ? pack_bf16x2(v[2 * q], v[(2 * q + 1) % kPerChunk]) : to_tf32(v[q]);
           sts128(arow + ((j ^ (arow_i & 7)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
         }
+      };
+      for (uint32_t sl = 0; sl < a.slabs; ++sl) {
+        mbar_wait(&a_empty[stage], phase ^ 1);
+#if IM2WIN_DIRECT_SPLIT_BUILD
+        if (sl + 1 < a.slabs) build_slab(sl, std::false_type{});
+        else build_slab(sl, std::true_type{});
+#else
+        build_slab(sl, std::true_type{});
+#endif
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_full[stage]);
