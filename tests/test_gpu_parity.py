@@ -547,3 +547,25 @@ def test_unaligned_and_degenerate_inputs(pad):
     o1 = pkg.conv_im2win_opt(xi, fi, p1)
     assert o1.dims == (1, 2, 1, 1)
     assert bits_equal_nan_as_class(o1.numpy(), orc.conv_direct(_pad_np(xi, pad), fi, 1))
+
+
+@pytest.mark.parametrize("group", ["1", "3", "5"])
+def test_tc_fused_tile_groups(group, layer_goldens, monkeypatch):
+    """The generic fused kernel's tile walk (runs of `group` consecutive tiles per CTA) covers
+    every tile exactly once: conv7 (two pieces per output row) and a ragged geometry."""
+    monkeypatch.setenv("IM2WIN_TILE_GROUP", group)
+    monkeypatch.setenv("IM2WIN_PHASE", "0")
+    monkeypatch.setenv("IM2WIN_SHIFT", "0")
+    g = layer_goldens["conv7"]
+    cfg = replace(BENCHMARKS["conv7"], batch=g["batch"], seed=g["seed"])
+    inp, flt = make_inputs(cfg)
+    ref = orc.conv_direct(inp, flt, cfg.stride)
+    out = pkg.conv_im2win_opt(inp, flt, cfg.params, variant="bf16", tc_path="fused").numpy()
+    assert pkg.normalized_max_diff(out, ref) <= TC_TOL["bf16"]
+    rng = np.random.default_rng(int(group))
+    inp = rng.standard_normal((3, 8, 9, 300), dtype=np.float32)
+    flt = rng.standard_normal((40, 8, 3, 3), dtype=np.float32)
+    ref = orc.conv_direct(inp, flt, 1)
+    for v in ("tf32", "bf16"):
+        out = pkg.conv_im2win_opt(inp, flt, pkg.ConvParams(8, 40, 3, 3, 1), variant=v, tc_path="fused").numpy()
+        assert pkg.normalized_max_diff(out, ref) <= TC_TOL[v], v

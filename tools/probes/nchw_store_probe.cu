@@ -165,6 +165,32 @@ __global__ void __launch_bounds__(256) pattern_bulk(float* out, int n, int co, i
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Variant: the kernels' lane-per-pixel pattern, but each CTA takes `group` consecutive tiles
+// (e.g. both halves of an output row) back to back instead of striding by gridDim.x
+__global__ void __launch_bounds__(256) pattern_grouped(float* out, int n, int co, int ho, int wo, int box_w, int group) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int quarter = warp % 4, half = warp / 4;
+  const int ow_tiles = (wo + box_w - 1) / box_w;
+  const long long tiles = (long long)n * ho * ow_tiles;
+  const int r = quarter * 32 + lane;
+  const long long hw = (long long)ho * wo;
+  for (long long t0 = (long long)blockIdx.x * group; t0 < tiles; t0 += (long long)gridDim.x * group) {
+    for (long long t = t0; t < t0 + group && t < tiles; ++t) {
+      const int owt = t % ow_tiles;
+      const long long rest = t / ow_tiles;
+      const int oh = rest % ho;
+      const long long img = rest / ho;
+      const int ow = owt * box_w + r;
+      if (r < box_w && ow < wo) {
+        float* base = out + img * co * hw + (long long)oh * wo + ow;
+        const int c0 = half * (co / 2);
+#pragma unroll 8
+        for (int c = 0; c < co / 2; ++c) base[(long long)(c0 + c) * hw] = (float)c;
+      }
+    }
+  }
+}
+
 __global__ void fill(float4* out, long long n4) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x)
     out[i] = make_float4(1.f, 2.f, 3.f, 4.f);
@@ -255,6 +281,13 @@ int main() {
       cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
       printf("bulk box_w=%d: %.3f ms  %.2f TB/s  (%s)\n", bw, ms, elems * 4 / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
     }
+  }
+  for (int g : {1, 2, 4, 8}) {
+    float ms;
+    pattern_grouped<<<148, 256>>>(out, n, co, ho, wo, 111, g);
+    cudaEventRecord(e0); pattern_grouped<<<148, 256>>>(out, n, co, ho, wo, 111, g); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+    printf("grouped box_w=111 group=%d: %.3f ms  %.2f TB/s\n", g, ms, elems * 4 / (ms * 1e-3) / 1e12);
   }
   fill<<<148 * 8, 256>>>((float4*)out, elems / 4);
   cudaEventRecord(e0);
