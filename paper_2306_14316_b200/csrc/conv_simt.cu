@@ -188,8 +188,7 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? 2 : ((BM / MT
       }
     }
     (void)full;
-    return;
-#endif
+#else
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
       const int c = tid + j * NT;
@@ -206,6 +205,7 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? 2 : ((BM / MT
         }
       }
     }
+#endif
   };
   auto load_stage = [&](int kt, int slot) {
     load_filter(kt, slot);
@@ -387,7 +387,7 @@ extern "C" int im2win_simt_pick(int M, long long n_gemm, int K) {
 // (all toggles compiled); 4-6: 4x4 micro-tiles (production toggles only).
 static const int kNumCfg = 7;
 static const int kBM[kNumCfg] = {128, 64, 96, 128, 64, 128, 32};
-static const int kBN[kNumCfg] = {128, 256, 128, 64, 64, 32, 128};
+// CTA tile N extents, for reference: {128, 256, 128, 64, 64, 32, 128}
 static const int kBKc[kNumCfg] = {16, 16, 16, 16, 16, 16, 16};
 static const int kMaxBK = 32;
 
@@ -488,7 +488,7 @@ namespace im2win {
 
 template <int STAGES, bool EXACT>
 __global__ void __launch_bounds__(256) conv_simt_1x1_kernel(const ConvArgs a) {
-  constexpr int BM = 16, BN = 16, BK = 8, NT = 256;
+  constexpr int BM = 16, BN = 16, BK = 8;
   __shared__ float As[STAGES][BK][BM];
   __shared__ float Bs[STAGES][BK][BN];
   __shared__ int64_t col_off[BN];

@@ -30,6 +30,10 @@ constexpr int kProducers = 256;
 constexpr int kProdWarps = kProducers / 32;
 constexpr int kDirEpiWarps = 4;
 constexpr int kDirColIters = 16;  // patch rows up to 512 floats (checked by plan_direct)
+#ifndef IM2WIN_DIRECT_LOADERS
+#define IM2WIN_DIRECT_LOADERS 1  // BF16: warps 9-11 fetch the input patches (mbarrier ring), producers only build
+#endif
+constexpr int kLoadWarps = 3;
 #ifndef IM2WIN_DIRECT_SPLIT_BUILD
 #define IM2WIN_DIRECT_SPLIT_BUILD 1  // padded-k check only in the last slab
 #endif
@@ -68,6 +72,63 @@ IM2WIN_DEVICE int4 lds128i(uint32_t addr) {
   return v;
 }
 
+// Patch columns are read in natural order (lane = column: coalesced) and stored phase-major
+// (column s*q + ph at ph*pcolq + q) so lanes later read consecutive words.  The smem offset
+// of column lane + 32*i is the same for every row of every tile: computed once per thread.
+struct PatchLanes {
+  uint32_t dst[kDirColIters];
+  uint32_t live;  // bit i: column lane + 32*i lies inside the patch row
+  IM2WIN_DEVICE PatchLanes(const DirectArgs& a, uint32_t lane) : live(0) {
+#pragma unroll
+    for (int i = 0; i < kDirColIters; ++i) {
+      const uint32_t col = lane + 32 * i;
+      dst[i] = 4 * ((col % a.stride) * a.pcolq + col / a.stride);
+      if (col < a.prow_pitch) live |= 1u << i;
+    }
+  }
+};
+
+// Rows w0, w0 + nw, ... of tile t's input patch -> shared buffer `pb` (4-byte cp.async,
+// zero-filled outside the image).
+IM2WIN_DEVICE void issue_patch_rows(const DirectArgs& a, const PatchLanes& pl, uint32_t t, uint32_t pb, uint32_t w0,
+                                    uint32_t nw, uint32_t lane) {
+  const uint32_t owt = t % a.ow_tiles;
+  const uint32_t rest = t / a.ow_tiles;
+  const uint32_t oh0 = (rest % a.oh_tiles) * a.rows;
+  const uint32_t img = rest / a.oh_tiles;
+  const int ih0 = static_cast<int>(oh0 * a.stride) - static_cast<int>(a.pad);
+  const int iw0 = static_cast<int>(owt * a.box_w * a.stride) - static_cast<int>(a.pad);
+  const float* xi = a.x + static_cast<int64_t>(img) * a.c_in * a.h_in * a.w_in;
+  uint32_t col_in = 0;  // bit i: column lane + 32*i is inside the image (this tile)
+#pragma unroll
+  for (int i = 0; i < kDirColIters; ++i) {
+    const int iw = iw0 + static_cast<int>(lane + 32 * i);
+    if (iw >= 0 && iw < static_cast<int>(a.w_in)) col_in |= 1u << i;
+  }
+  col_in &= pl.live;
+  const uint32_t prows_total = a.c_in * a.prow;
+  uint32_t c = w0 / a.prow, rr = w0 % a.prow;
+  for (uint32_t pr = w0; pr < prows_total; pr += nw) {
+    const int ih = ih0 + static_cast<int>(rr);
+    const bool in_row = ih >= 0 && ih < static_cast<int>(a.h_in);
+    const uint32_t m = in_row ? col_in : 0u;
+    const float* src = xi + (static_cast<int64_t>(c) * a.h_in + (in_row ? ih : 0)) * a.w_in + iw0 + lane;
+    const uint32_t dst_row = pb + pr * a.prow_pitch * 4;
+#pragma unroll
+    for (int i = 0; i < kDirColIters; ++i) {
+      if ((pl.live >> i) & 1u) {
+        const bool ok = (m >> i) & 1u;
+        cp_async_4_zfill(dst_row + pl.dst[i], ok ? src + 32 * i : xi, !ok);
+      }
+    }
+    rr += nw;
+    while (rr >= a.prow) {
+      rr -= a.prow;
+      ++c;
+    }
+  }
+}
+
 template <bool BF16, int N, int STAGES>
 __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const DirectArgs a) {
   constexpr int kBK = BF16 ? 64 : 32;
@@ -76,6 +137,9 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
   constexpr uint32_t kATile = kTileM * kRowBytes;
   constexpr uint32_t kTmemCols = (2 * N <= 128) ? 128 : (2 * N <= 256 ? 256 : 512);
   constexpr uint32_t kIdesc = instr_desc<BF16, N>();
+  // measured (tools/direct_ab.py, N=128): loader warps +7% (conv1) to +22% (conv7) for BF16;
+  // TF32 (twice the slabs: the build is the bound) loses 11%, so it keeps in-line fetching
+  constexpr bool kLoaders = IM2WIN_DIRECT_LOADERS && BF16;
 
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t a_full[STAGES];
@@ -83,6 +147,8 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
   __shared__ __align__(8) uint64_t tfull_bar[2];
   __shared__ __align__(8) uint64_t tempty_bar[2];
   __shared__ __align__(8) uint64_t b_ready;
+  __shared__ __align__(8) uint64_t p_full[4];   // patch buffer landed (loader threads' cp.async)
+  __shared__ __align__(8) uint64_t p_empty[4];  // patch buffer built from (producer warps)
   __shared__ uint32_t tmem_base_sh;
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -105,6 +171,10 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
       mbar_init(&tempty_bar[s], kDirEpiWarps);
     }
     mbar_init(&b_ready, kProdWarps);
+    for (int b = 0; b < 4; ++b) {
+      mbar_init(&p_full[b], kLoadWarps * 32);
+      mbar_init(&p_empty[b], kProdWarps);
+    }
     fence_barrier_init();
   }
   if (warp == 9) {
@@ -151,78 +221,37 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
     // pixel (r_row, r_col) reads patch rows r_row*s + fh, columns r_col*s + fw = phase fw%s, index r_col + fw/s
     // rows past the tile's pixels build from pixel 0 (in-bounds reads; the epilogue drops them)
     const uint32_t pix_base = row_ok ? (r_row * a.stride) * a.prow_pitch + r_col : 0u;
-    const uint32_t prows_total = a.c_in * a.prow;
-    // Patch columns are read in natural order (lane = column: coalesced) and stored phase-major
-    // (column s*q + ph at ph*pcolq + q) so lanes later read consecutive words.  The smem offset
-    // of column lane + 32*i is the same for every row of every tile: computed once.
-    uint32_t col_dst[kDirColIters];
-    uint32_t col_live = 0;  // bit i: column lane + 32*i lies inside the patch row
-#pragma unroll
-    for (int i = 0; i < kDirColIters; ++i) {
-      const uint32_t col = lane + 32 * i;
-      col_dst[i] = 4 * ((col % a.stride) * a.pcolq + col / a.stride);
-      if (col < a.prow_pitch) col_live |= 1u << i;
-    }
-    // patch of tile t -> buffer at smem address `pb`: 4-byte cp.async, zero-filled outside the image
+    const PatchLanes pl(a, lane);
     auto issue_patch = [&](uint32_t t, uint32_t pb) {
-      const uint32_t owt = t % a.ow_tiles;
-      const uint32_t rest = t / a.ow_tiles;
-      const uint32_t oh0 = (rest % a.oh_tiles) * a.rows;
-      const uint32_t img = rest / a.oh_tiles;
-      const int ih0 = static_cast<int>(oh0 * a.stride) - static_cast<int>(a.pad);
-      const int iw0 = static_cast<int>(owt * a.box_w * a.stride) - static_cast<int>(a.pad);
-      const float* xi = a.x + static_cast<int64_t>(img) * a.c_in * a.h_in * a.w_in;
-      uint32_t col_in = 0;  // bit i: column lane + 32*i is inside the image (this tile)
-#pragma unroll
-      for (int i = 0; i < kDirColIters; ++i) {
-        const int iw = iw0 + static_cast<int>(lane + 32 * i);
-        if (iw >= 0 && iw < static_cast<int>(a.w_in)) col_in |= 1u << i;
-      }
-      col_in &= col_live;
-      uint32_t c = warp / a.prow, rr = warp % a.prow;
-      for (uint32_t pr = warp; pr < prows_total; pr += kProdWarps) {
-        const int ih = ih0 + static_cast<int>(rr);
-        const bool in_row = ih >= 0 && ih < static_cast<int>(a.h_in);
-        const uint32_t m = in_row ? col_in : 0u;
-        const float* src = xi + (static_cast<int64_t>(c) * a.h_in + (in_row ? ih : 0)) * a.w_in + iw0 + lane;
-        const uint32_t dst_row = pb + pr * a.prow_pitch * 4;
-#pragma unroll
-        for (int i = 0; i < kDirColIters; ++i) {
-          if ((col_live >> i) & 1u) {
-            const bool ok = (m >> i) & 1u;
-            cp_async_4_zfill(dst_row + col_dst[i], ok ? src + 32 * i : xi, !ok);
-          }
-        }
-        rr += kProdWarps;
-        while (rr >= a.prow) {
-          rr -= a.prow;
-          ++c;
-        }
-      }
+      issue_patch_rows(a, pl, t, pb, warp, kProdWarps, lane);
       cp_async_commit();
     };
     // patch_bufs buffers: the patch of tile it + (bufs - 1) is fetched while tile it is built
     const uint32_t nb = a.patch_bufs;
     auto pbuf = [&](uint32_t i) { return patch_s + (i % nb) * patch_elems * 4; };
+    if (!kLoaders)
     for (uint32_t d = 0; d + 1 < nb; ++d) {
       const uint32_t tt = blockIdx.x + d * gridDim.x;
       if (tt < a.tiles) issue_patch(tt, pbuf(d));
       else cp_async_commit();
     }
-    if (nb == 1 && blockIdx.x < a.tiles) issue_patch(blockIdx.x, pbuf(0));
+    if (!kLoaders && nb == 1 && blockIdx.x < a.tiles) issue_patch(blockIdx.x, pbuf(0));
     uint32_t stage = 0, phase = 0, it = 0;
     for (uint32_t t = blockIdx.x; t < a.tiles; t += gridDim.x, ++it) {
       const uint32_t pb = pbuf(it);
+      if constexpr (kLoaders) {
+        mbar_wait(&p_full[it % nb], (it / nb) & 1);  // this tile's patch has landed
+      } else {
       // this tile's group is the oldest pending one: allow nb - 2 newer groups in flight
       if (nb >= 4) cp_async_wait<2>();
       else if (nb == 3) cp_async_wait<1>();
       else cp_async_wait<0>();
       named_sync_producers();  // this tile's patch has landed for every producer
-      const uint32_t next = t + gridDim.x;
       if (nb > 1) {
         const uint32_t ahead = t + (nb - 1) * gridDim.x;  // buffer (it - 1) % nb: its rows were built
         if (ahead < a.tiles) issue_patch(ahead, pbuf(it + nb - 1));
         else cp_async_commit();
+      }
       }
       const uint32_t my_base = pb + 4 * pix_base;
       // one slab: this thread's four 16-byte chunks of its A row; only the last slab holds
@@ -266,11 +295,26 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
         if (lane == 0) mbar_arrive(&a_full[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (nb == 1 && next < a.tiles) {
+      if constexpr (kLoaders) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_empty[it % nb]);  // this warp's rows are built: buffer reusable
+      } else if (nb == 1 && t + gridDim.x < a.tiles) {
         named_sync_producers();  // every row built from the single buffer
-        issue_patch(next, pbuf(0));
+        issue_patch(t + gridDim.x, pbuf(0));
       }
     }
+  } else if (kLoaders && warp >= 9 && warp < 9 + kLoadWarps) {
+    // ------------------------------------------------------------- patch loaders
+    const PatchLanes pl(a, lane);
+    const uint32_t nb = a.patch_bufs;
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < a.tiles; t += gridDim.x, ++it) {
+      const uint32_t b = it % nb;
+      if (it >= nb) mbar_wait(&p_empty[b], ((it / nb) - 1) & 1);
+      issue_patch_rows(a, pl, t, patch_s + b * patch_elems * 4, warp - 9, kLoadWarps, lane);
+      cp_async_arrive_noinc(&p_full[b]);
+    }
+    cp_async_wait<0>();
   } else if (warp == 8) {
     // ------------------------------------------------------------- MMA issuer
     if (lane == 0) {
