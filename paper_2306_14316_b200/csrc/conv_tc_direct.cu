@@ -25,9 +25,17 @@
 namespace im2win {
 namespace tc {
 
-constexpr int kDirThreads = 16 * 32;
-constexpr int kProducers = 256;
-constexpr int kProdWarps = kProducers / 32;
+#ifndef IM2WIN_DIRECT_PROD_WARPS
+#define IM2WIN_DIRECT_PROD_WARPS 8
+#endif
+// warps [0, P): producers; P: MMA issuer; P+1: TMEM allocator (+ loader); P+1..P+3: patch
+// loaders (BF16); the last 4: epilogue (warp % 4 = TMEM lane quarter).
+constexpr int kProdWarps = IM2WIN_DIRECT_PROD_WARPS;
+constexpr int kProducers = kProdWarps * 32;
+constexpr int kDirWarps = kProdWarps + 8;
+constexpr int kDirThreads = kDirWarps * 32;
+constexpr int kChunksPerThread = 8 * kTileM / kProducers;  // 16-byte chunks of its A row per slab
+static_assert(kDirWarps % 4 == 0, "the epilogue warps must cover the four TMEM lane quarters");
 constexpr int kDirEpiWarps = 4;
 constexpr int kDirColIters = 16;  // patch rows up to 512 floats (checked by plan_direct)
 #ifndef IM2WIN_DIRECT_LOADERS
@@ -177,7 +185,7 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
     }
     fence_barrier_init();
   }
-  if (warp == 9) {
+  if (warp == kProdWarps + 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -190,7 +198,7 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
   if (warp < kProdWarps) {
     // ------------------------------------------------------------- producers
     const uint32_t tid = threadIdx.x;
-    const uint32_t arow_i = tid % kTileM, half = tid / kTileM;  // A row, chunk half (j = 4*half .. 4*half+3)
+    const uint32_t arow_i = tid % kTileM, half = tid / kTileM;  // A row, chunk group (j = kCPT*half + jj)
     // resident filter: slab sl, row m, 16-byte chunk j -> swizzled chunk j ^ (m & 7)
     {
       const uint4* src = static_cast<const uint4*>(a.bpk);
@@ -260,8 +268,8 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
         const uint32_t arow = smem_u32(a_ring + stage * kATile) + arow_i * kRowBytes;
         const uint32_t ko = koff_s + 4 * sl * kBK;
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int j = 4 * half + jj;
+        for (int jj = 0; jj < kChunksPerThread; ++jj) {
+          const int j = kChunksPerThread * half + jj;
           // this chunk's kPerChunk window offsets (warp-uniform: broadcast loads)
           int off[8];
           const int4 o_lo = lds128i(ko + 4 * (j * kPerChunk));
@@ -303,7 +311,7 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
         issue_patch(t + gridDim.x, pbuf(0));
       }
     }
-  } else if (kLoaders && warp >= 9 && warp < 9 + kLoadWarps) {
+  } else if (kLoaders && warp >= kProdWarps + 1 && warp < kProdWarps + 1 + kLoadWarps) {
     // ------------------------------------------------------------- patch loaders
     const PatchLanes pl(a, lane);
     const uint32_t nb = a.patch_bufs;
@@ -311,11 +319,11 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
     for (uint32_t t = blockIdx.x; t < a.tiles; t += gridDim.x, ++it) {
       const uint32_t b = it % nb;
       if (it >= nb) mbar_wait(&p_empty[b], ((it / nb) - 1) & 1);
-      issue_patch_rows(a, pl, t, patch_s + b * patch_elems * 4, warp - 9, kLoadWarps, lane);
+      issue_patch_rows(a, pl, t, patch_s + b * patch_elems * 4, warp - kProdWarps - 1, kLoadWarps, lane);
       cp_async_arrive_noinc(&p_full[b]);
     }
     cp_async_wait<0>();
-  } else if (warp == 8) {
+  } else if (warp == kProdWarps) {
     // ------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       mbar_wait(&b_ready, 0);
@@ -342,7 +350,7 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (warp >= 16 - kDirEpiWarps) {
+  } else if (warp >= kDirWarps - kDirEpiWarps) {
     // ------------------------------------------------------------- epilogue
     const int quarter = warp % 4;
     const uint32_t r = quarter * 32 + lane;
@@ -378,7 +386,7 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == kProdWarps + 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(kTmemCols));
   }
