@@ -272,10 +272,16 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU over NCCL; IM2WIN_DIST_BACKEND=gloo lets several ranks share one GPU
+    # (exercises the multi-rank path -- barrier, max over ranks, rank-0 line -- on a 1-GPU box)
+    backend = os.environ.get("IM2WIN_DIST_BACKEND", "nccl")
+    dev = torch.device("cuda", local_rank % torch.cuda.device_count() if world > 1 else 0)
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    dev = torch.device("cuda", local_rank if world > 1 else 0)
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(dev)
     set_fp32_precision("ieee")
 
@@ -286,7 +292,7 @@ def main() -> None:
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
