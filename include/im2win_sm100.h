@@ -59,7 +59,9 @@ typedef struct im2win_tile_plan {
 /* Window-order transform (layouts.py:73-95).
  * src: (n, c, h, w) float32; dst: (n, c, h_out, h_f * w_eff) float32 where
  * h_out = (h - h_f) / stride + 1, w_eff = (w_out - 1) * stride + w_f.
- * Bit-exact copy: dst[i,r,m,col*h_f+u] = src[i,r,m*stride+u,col]. */
+ * Bit-exact copy: dst[i,r,m,col*h_f+u] = src[i,r,m*stride+u,col].
+ * Any 4-byte aligned src/dst (numpy/torch views at an element offset included); 16-byte
+ * aligned buffers take the TMA bulk-copy kernel. */
 int im2win_transform_f32(const float* src, float* dst, int64_t n, int64_t c, int64_t h,
                          int64_t w, int32_t h_f, int32_t w_f, int32_t stride, void* stream);
 
@@ -73,7 +75,8 @@ int im2win_transform_f32_padded(const float* src, float* dst, int64_t n, int64_t
                                 int64_t w, int32_t h_f, int32_t w_f, int32_t stride, int32_t pad,
                                 void* stream);
 
-/* Bytes of device workspace im2win_conv_f32 needs (packed filter + offsets). */
+/* Bytes of device workspace im2win_conv_f32 needs (packed filter + offsets); the
+ * workspace must be 16-byte aligned. */
 size_t im2win_conv_workspace_bytes(int64_t c_in, int64_t c_out, int32_t h_f, int32_t w_f,
                                    int32_t variant);
 

@@ -482,6 +482,10 @@ bool plan_direct(int64_t n, int64_t c_in, int64_t h, int64_t w, int64_t c_out, i
   // deepest patch prefetch (up to 4 buffers) and A ring (2-4 stages) that fit
   p.stages = 4;
   a.patch_bufs = 4;
+  if (const char* pb_env = getenv("IM2WIN_DIRECT_BUFS")) {  // A/B: patch buffers first, A stages to fit
+    a.patch_bufs = static_cast<uint32_t>(std::min(4, std::max(1, atoi(pb_env))));
+    while (need(p.stages, a.patch_bufs) > budget && p.stages > 2) --p.stages;
+  }
   while (need(p.stages, a.patch_bufs) > budget && a.patch_bufs > 2) --a.patch_bufs;
   while (need(p.stages, a.patch_bufs) > budget && p.stages > 2) --p.stages;
   if (need(p.stages, a.patch_bufs) > budget) a.patch_bufs = 1;
