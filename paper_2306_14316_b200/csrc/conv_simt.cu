@@ -23,6 +23,8 @@
 //     (the reference's hoisted src_off/delta, optimized.py:42, :101-102);
 //   * register micro-kernel: each thread owns an 8x8 tile split into two 4x4
 //     quadrants so fragments are 128-bit shared loads ("vectorized load").
+#include <algorithm>
+
 #include "common.cuh"
 
 #ifndef IM2WIN_SIMT_BRANCHLESS
@@ -33,6 +35,12 @@
 #endif
 #ifndef IM2WIN_SIMT_PART_ROWS
 #define IM2WIN_SIMT_PART_ROWS 4  // window rows gathered per interleaved hook
+#endif
+#ifndef IM2WIN_SIMT_SMALLK
+#define IM2WIN_SIMT_SMALLK 1  // persistent small-K kernel for K <= 64, Co <= 64 (conv7)
+#endif
+#ifndef IM2WIN_SIMT_SMALLK_UNROLL
+#define IM2WIN_SIMT_SMALLK_UNROLL 4
 #endif
 #ifndef IM2WIN_SIMT_INTERLEAVE
 #define IM2WIN_SIMT_INTERLEAVE 1
@@ -337,6 +345,145 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? 2 : ((BM / MT
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Small-K persistent variant (K <= 64, Co <= 64: conv7, K = 27).  With one or two
+// K-slabs per tile the per-CTA prologue (first gathers) and epilogue (output stores)
+// dominate a 64x256 CTA's life.  Here each CTA keeps its filter panel resident and
+// walks n-tiles: the window gather of tile i+1 is in flight while tile i is computed
+// and stored.  Same micro-tile, same arithmetic (FMUL+FADD in ascending k from +0),
+// and the k loop stops at K instead of the padded Kp.
+// ---------------------------------------------------------------------------
+template <int KP, bool EXACT>
+__global__ void __launch_bounds__(256, 2) conv_simt_smallk_kernel(const ConvArgs a) {
+  constexpr int BM = 64, BN = 256, MT = 8, NT = 256, TXN = BN / MT;
+  constexpr int kUnroll = IM2WIN_SIMT_SMALLK_UNROLL;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* As = reinterpret_cast<float*>(smem_raw);  // [KP][BM], resident
+  float* Bs = As + KP * BM;                         // [2][KP][BN]
+  int* sdelta = reinterpret_cast<int*>(Bs + 2 * KP * BN);  // [KP]
+  const int tid = threadIdx.x;
+  for (int q = tid; q < KP * BM / 4; q += NT)
+    reinterpret_cast<float4*>(As)[q] = __ldg(reinterpret_cast<const float4*>(a.fltT) + q);  // Mp == BM
+  for (int q = tid; q < KP; q += NT) sdelta[q] = __ldg(a.delta + q);
+  __syncthreads();
+
+  const uint32_t n_tiles = (a.n_gemm + BN - 1) / BN;
+  // gather of tile `t` into buffer `b`: this thread owns column n0 + tid (all KP rows)
+  auto issue = [&](uint32_t t, int b) {
+    const uint32_t n = t * BN + tid;
+    const float* src = a.win;
+    bool zero = true;
+    if (n < a.n_gemm) {
+      uint32_t img, rem, oh, ow;
+      a.fd_hw.divmod(n, img, rem);
+      a.fd_wo.divmod(rem, oh, ow);
+      src = a.win + (static_cast<int64_t>(img) * a.c_in * a.h_out + oh) * a.row_len + static_cast<int64_t>(ow) * a.s_hf;
+      zero = false;
+    }
+    float* dst = Bs + b * KP * BN + tid;
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      const int d = sdelta[k];
+      const bool ok = d >= 0;
+      cp_async_4_zfill(smem_u32(dst + k * BN), src + (ok ? d : 0), zero || !ok);
+    }
+    cp_async_commit();
+  };
+  const int tx = tid % TXN, ty = tid / TXN;
+  uint32_t t = blockIdx.x;
+  if (t < n_tiles) issue(t, 0);
+  for (int it = 0; t < n_tiles; t += gridDim.x, ++it) {
+    const int b = it & 1;
+    const uint32_t tn = t + gridDim.x;
+    if (tn < n_tiles) issue(tn, b ^ 1);  // its buffer was released by the barrier after compute(it-1)
+    else cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    float acc[MT][MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < MT; ++j) acc[i][j] = 0.0f;
+    const float* bs = Bs + b * KP * BN;
+    // k loop to K (padded k never computed), unrolled by 4 only: a fully unrolled KP-step
+    // body misses in the instruction cache (ncu: no_instruction stalls)
+#pragma unroll kUnroll
+    for (int kk = 0; kk < a.K; ++kk) {
+      {
+        float fa[MT], fb[MT];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float4 av = *reinterpret_cast<const float4*>(As + kk * BM + h * (BM / 2) + ty * 4);
+          const float4 bv = *reinterpret_cast<const float4*>(bs + kk * BN + h * (BN / 2) + tx * 4);
+          fa[4 * h] = av.x; fa[4 * h + 1] = av.y; fa[4 * h + 2] = av.z; fa[4 * h + 3] = av.w;
+          fb[4 * h] = bv.x; fb[4 * h + 1] = bv.y; fb[4 * h + 2] = bv.z; fb[4 * h + 3] = bv.w;
+        }
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < MT; ++j) acc[i][j] = mac<EXACT>(acc[i][j], fa[i], fb[j]);
+      }
+    }
+    __syncthreads();  // buffer b is free for the gather of tile it + 2
+    // epilogue (optimized.py:209-214), overlapped with the gather in flight
+    const uint32_t n0 = t * BN;
+#pragma unroll
+    for (int hj = 0; hj < 2; ++hj) {
+      const uint32_t nq = n0 + hj * (BN / 2) + tx * 4;
+      if (a.vec_out && nq + 3 < a.n_gemm) {
+        uint32_t img, rem;
+        a.fd_hw.divmod(nq, img, rem);
+        float* base = a.out + static_cast<int64_t>(img) * a.M * a.hw + rem;
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int m = (i / 4) * (BM / 2) + ty * 4 + (i % 4);
+          if (m < a.M)
+            __stcs(reinterpret_cast<float4*>(base + static_cast<int64_t>(m) * a.hw),
+                   make_float4(acc[i][4 * hj], acc[i][4 * hj + 1], acc[i][4 * hj + 2], acc[i][4 * hj + 3]));
+        }
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const uint32_t n = nq + jj;
+          if (n >= a.n_gemm) continue;
+          uint32_t img, rem;
+          a.fd_hw.divmod(n, img, rem);
+          float* base = a.out + static_cast<int64_t>(img) * a.M * a.hw + rem;
+#pragma unroll
+          for (int i = 0; i < MT; ++i) {
+            const int m = (i / 4) * (BM / 2) + ty * 4 + (i % 4);
+            if (m < a.M) base[static_cast<int64_t>(m) * a.hw] = acc[i][4 * hj + jj];
+          }
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <int KP, bool EXACT>
+static cudaError_t launch_smallk(const ConvArgs& a, cudaStream_t stream) {
+  const size_t smem = (static_cast<size_t>(KP) * 64 + 2ull * KP * 256) * 4 + KP * 4;
+  auto kern = conv_simt_smallk_kernel<KP, EXACT>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+  if (occ < 1) occ = 1;
+  const uint64_t n_tiles = (static_cast<uint64_t>(a.n_gemm) + 255) / 256;
+  const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(n_tiles, static_cast<uint64_t>(occ) * sms));
+  kern<<<grid, 256, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+
+
 // ---------------------------------------------------------------------------
 // Tile configurations compiled into the library.
 // ---------------------------------------------------------------------------
@@ -403,6 +550,7 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
     *err = "im2win_conv_f32: extents exceed the kernel's index range";
     return 1;
   }
+  const bool auto_cfg = cfg < 0;
   if (cfg < 0) cfg = im2win_simt_pick(static_cast<int>(c_out), n_gemm, static_cast<int>(K));
   if (cfg >= kNumCfg) {
     *err = "im2win_conv_f32: unknown tile configuration";
@@ -454,6 +602,19 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
 #define IM2WIN_DISPATCH4(BM_, BN_, BK_)                                                             \
   if (exact) e = launch_cfg<BM_, BN_, BK_, 3, true, true, 4>(a, stream);                            \
   else e = launch_cfg<BM_, BN_, BK_, 3, false, true, 4>(a, stream);
+  // small K (conv7): the persistent kernel with a resident filter and the next tile's gather
+  // in flight (library choice only; an explicit TilePlan keeps its CTA tile)
+  const bool smallk = IM2WIN_SIMT_SMALLK && auto_cfg && cfg == 1 && vec && stages > 1 && c_out <= 64 && K <= 64 &&
+                      (n_gemm + 255) / 256 >= 8LL * 148 * 2;
+  if (smallk) {
+    im2win_note_kernel("conv_simt_smallk_kernel (8x8 micro-tiles, persistent, resident filter)");
+    switch (Kp) {
+      case 16: e = exact ? launch_smallk<16, true>(a, stream) : launch_smallk<16, false>(a, stream); break;
+      case 32: e = exact ? launch_smallk<32, true>(a, stream) : launch_smallk<32, false>(a, stream); break;
+      case 48: e = exact ? launch_smallk<48, true>(a, stream) : launch_smallk<48, false>(a, stream); break;
+      default: e = exact ? launch_smallk<64, true>(a, stream) : launch_smallk<64, false>(a, stream); break;
+    }
+  } else
   switch (cfg) {
     case 0: { IM2WIN_DISPATCH(128, 128, 16) break; }
     case 1: { IM2WIN_DISPATCH(64, 256, 16) break; }

@@ -569,3 +569,27 @@ def test_tc_fused_tile_groups(group, layer_goldens, monkeypatch):
     for v in ("tf32", "bf16"):
         out = pkg.conv_im2win_opt(inp, flt, pkg.ConvParams(8, 40, 3, 3, 1), variant=v, tc_path="fused").numpy()
         assert pkg.normalized_max_diff(out, ref) <= TC_TOL[v], v
+
+
+@pytest.mark.parametrize("variant", ["fp32-exact", "fp32-fma"])
+def test_simt_smallk_persistent_kernel(variant):
+    """The persistent small-K SIMT kernel (library choice for K <= 64, Co <= 64 with enough
+    tiles: conv7) gives the bits of the tiled kernel (explicit 64x256 plan) and of the oracle,
+    including special values, a ragged last tile and odd K (padded k never computed)."""
+    from paper_2306_14316_b200 import _lib
+    for (n, c, h, w, co, hf, wf) in [(16, 3, 224, 224, 64, 3, 3), (20, 5, 161, 203, 40, 3, 3), (32, 7, 130, 150, 64, 2, 3)]:
+        rng = np.random.default_rng(n * 100 + c)
+        inp = rng.standard_normal((n, c, h, w), dtype=np.float32)
+        inp[0, 0, 0, :5] = [np.inf, -np.inf, np.nan, 0.0, -0.0]
+        flt = rng.standard_normal((co, c, hf, wf), dtype=np.float32)
+        params = pkg.ConvParams(c, co, hf, wf, 1)
+        win = pkg.im2win(torch.from_numpy(inp).to(DEV), params)
+        out = pkg.compute_from_windows_opt(win, torch.from_numpy(flt).to(DEV), params, variant=variant)
+        assert "smallk" in _lib.last_kernel(), _lib.last_kernel()
+        tiled = pkg.compute_from_windows_opt(win, torch.from_numpy(flt).to(DEV), params,
+                                             pkg.TilePlan(64, 256, 8, 8, 8), variant=variant)
+        assert bits_equal_nan_as_class(out.numpy(), tiled.numpy()), (n, c, h, w)
+        if variant == "fp32-exact":
+            for i in (0, n - 1):
+                ref = orc.conv_direct(inp[i:i + 1], flt, 1)
+                assert bits_equal_nan_as_class(out.data[i:i + 1].cpu().numpy(), ref), (n, c, h, w, i)
