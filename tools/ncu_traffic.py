@@ -37,7 +37,7 @@ def val(r, i, table):
 launches = [(r[ki], val(r, rd, scale) + val(r, wr, scale), val(r, dur, tscale)) for r in data]
 names = list(BENCHMARKS)
 assert len(launches) == 2 * len(names), f"expected {2 * len(names)} launches, got {len(launches)}"
-out = {"capture": "ncu --set full --clock-control none -k regex:'conv_simt_kernel|im2win_transform_pipe' "
+out = {"capture": "ncu --set full --clock-control none -k regex:'conv_simt|im2win_transform_pipe' "
                   f"python tools/run_all_layers.py --batch {batch} --variant {variant}",
        "batch": batch, "variant": variant, "layers": {}}
 for i, name in enumerate(names):
