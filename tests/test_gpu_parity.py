@@ -577,7 +577,8 @@ def test_simt_smallk_persistent_kernel(variant):
     tiles: conv7) gives the bits of the tiled kernel (explicit 64x256 plan) and of the oracle,
     including special values, a ragged last tile and odd K (padded k never computed)."""
     from paper_2306_14316_b200 import _lib
-    for (n, c, h, w, co, hf, wf) in [(16, 3, 224, 224, 64, 3, 3), (20, 5, 161, 203, 40, 3, 3), (32, 7, 130, 150, 64, 2, 3)]:
+    for (n, c, h, w, co, hf, wf) in [(16, 3, 224, 224, 64, 3, 3), (20, 5, 161, 203, 40, 3, 3), (32, 7, 130, 150, 64, 2, 3),
+                                          (20, 1, 180, 180, 32, 4, 4), (14, 4, 212, 212, 64, 4, 4)]:
         rng = np.random.default_rng(n * 100 + c)
         inp = rng.standard_normal((n, c, h, w), dtype=np.float32)
         inp[0, 0, 0, :5] = [np.inf, -np.inf, np.nan, 0.0, -0.0]
