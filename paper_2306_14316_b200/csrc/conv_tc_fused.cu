@@ -108,26 +108,29 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_wide_kernel(const float* __r
       row[0] = v[j].x; row[1] = v[j].y; row[2] = v[j].z; row[3] = v[j].w;
     }
     __syncthreads();
-    // store: 4 threads per pixel, 16 consecutive channels each
-    const uint32_t pl = t / 4, cq = t % 4;
-    const uint32_t p = p0 + pl;
-    if (p < hw) {
-      const uint64_t o = pm.pixel(img, p) * c_pad;
+    // store: kPer threads per pixel, one 16-byte granule (G channels) each, granule fastest:
+    // a warp instruction writes contiguous pixel rows (512 B), no partial sectors
+    constexpr uint32_t G = BF16 ? 8 : 4;
+    constexpr uint32_t kPer = 64 / G;         // threads per pixel
+    constexpr uint32_t kPass = 256 / kPer;    // pixels per pass
+    const uint32_t cq = t % kPer;
+    const uint32_t cl = cq * G, c = c0 + cl;
 #pragma unroll
-      for (int g = 0; g < 16; g += (BF16 ? 8 : 4)) {
-        const uint32_t cl = cq * 16 + g, c = c0 + cl;
-        if (c < c_pad) {
-          if constexpr (BF16) {
-            uint4 q;
-            q.x = pack_bf16x2(tile[cl][pl], tile[cl + 1][pl]);
-            q.y = pack_bf16x2(tile[cl + 2][pl], tile[cl + 3][pl]);
-            q.z = pack_bf16x2(tile[cl + 4][pl], tile[cl + 5][pl]);
-            q.w = pack_bf16x2(tile[cl + 6][pl], tile[cl + 7][pl]);
-            __stcs(reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dst) + o + c), q);
-          } else {
-            __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + o + c),
-                   make_float4(tile[cl][pl], tile[cl + 1][pl], tile[cl + 2][pl], tile[cl + 3][pl]));
-          }
+    for (uint32_t pp = 0; pp < 64; pp += kPass) {
+      const uint32_t pl = pp + t / kPer;
+      const uint32_t p = p0 + pl;
+      if (p < hw && c < c_pad) {
+        const uint64_t o = pm.pixel(img, p) * c_pad;
+        if constexpr (BF16) {
+          uint4 q;
+          q.x = pack_bf16x2(tile[cl][pl], tile[cl + 1][pl]);
+          q.y = pack_bf16x2(tile[cl + 2][pl], tile[cl + 3][pl]);
+          q.z = pack_bf16x2(tile[cl + 4][pl], tile[cl + 5][pl]);
+          q.w = pack_bf16x2(tile[cl + 6][pl], tile[cl + 7][pl]);
+          __stcs(reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dst) + o + c), q);
+        } else {
+          __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + o + c),
+                 make_float4(tile[cl][pl], tile[cl + 1][pl], tile[cl + 2][pl], tile[cl + 3][pl]));
         }
       }
     }
