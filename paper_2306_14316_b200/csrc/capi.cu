@@ -283,10 +283,11 @@ int32_t im2win_conv_direct_supported(int64_t n, int64_t c_in, int64_t h, int64_t
 // stride-4 layers) or a tiny window (K <= 32) -- and loses elsewhere (7x7 stride 2; TF32).
 int32_t im2win_conv_direct_preferred(int64_t n, int64_t c_in, int64_t h, int64_t w, int64_t c_out, int32_t h_f,
                                      int32_t w_f, int32_t stride, int32_t pad, int32_t variant) {
-  if (variant != IM2WIN_BF16) return 0;
+  if (variant != IM2WIN_BF16 && variant != IM2WIN_TF32) return 0;
   if (!im2win_conv_direct_supported(n, c_in, h, w, c_out, h_f, w_f, stride, pad, variant)) return 0;
-  // measured (tools/tc_kernels.py, N=128, BF16): conv1/conv2 (Wo 55-56) 155-161 TF direct vs 116-120
-  // TF through the channels-last copy; wide outputs (conv3, conv7) are faster through the copy
+  // measured (bench.py, N=128, copy + conv vs direct): conv1/conv2 (Wo 55-56) BF16 166-173 TF direct vs
+  // 116-120 through the channels-last copy, TF32 111-116 vs 97-103; wide outputs (conv3, conv7) are
+  // faster through the copy
   const int64_t w_out = (w + 2 * pad - w_f) / stride + 1;
   return w_out <= 64 ? 1 : 0;
 }
