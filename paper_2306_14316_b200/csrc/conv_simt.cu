@@ -62,6 +62,7 @@ struct ConvArgs {
   FastDiv fd_hw, fd_wo;
   uint32_t m_tiles;
   uint32_t vec_out;                 // Ho*Wo % 4 == 0: 16-byte output stores
+  uint32_t n_base;                  // first GEMM column of this launch (tail launches)
 };
 
 // ---------------------------------------------------------------------------
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? 2 : ((BM / MT
   const uint32_t m_tile = blockIdx.x % a.m_tiles;
   const uint32_t n_tile = blockIdx.x / a.m_tiles;
   const int m0 = m_tile * BM;
-  const uint32_t n0 = n_tile * BN;
+  const uint32_t n0 = a.n_base + n_tile * BN;
 
   if constexpr (SD) {
     for (int q = tid; q < a.Kp / 4; q += NT)
@@ -497,7 +498,7 @@ template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC, int MT>
 static cudaError_t launch_cfg(const ConvArgs& a0, cudaStream_t stream) {
   ConvArgs a = a0;
   a.m_tiles = (a.M + BM - 1) / BM;
-  uint64_t n_tiles = (static_cast<uint64_t>(a.n_gemm) + BN - 1) / BN;
+  uint64_t n_tiles = (static_cast<uint64_t>(a.n_gemm - a.n_base) + BN - 1) / BN;
   uint64_t grid = n_tiles * a.m_tiles;
   const bool sd = static_cast<size_t>(a.Kp) * 4 <= kDeltaSmemMax;
   size_t smem = static_cast<size_t>(STAGES) * BK * (BM + BN) * 4 + (sd ? static_cast<size_t>(a.Kp) * 4 : 0);
@@ -614,16 +615,57 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
       case 48: e = exact ? launch_smallk<48, true>(a, stream) : launch_smallk<48, false>(a, stream); break;
       default: e = exact ? launch_smallk<64, true>(a, stream) : launch_smallk<64, false>(a, stream); break;
     }
-  } else
-  switch (cfg) {
-    case 0: { IM2WIN_DISPATCH(128, 128, 16) break; }
-    case 1: { IM2WIN_DISPATCH(64, 256, 16) break; }
-    case 2: { IM2WIN_DISPATCH(96, 128, 16) break; }
-    case 3: { IM2WIN_DISPATCH(128, 64, 16) break; }
-    case 4: { IM2WIN_DISPATCH4(64, 64, 16) break; }
-    case 5: { IM2WIN_DISPATCH4(128, 32, 16) break; }
-    case 6: { IM2WIN_DISPATCH4(32, 128, 16) break; }
-    default: *err = "im2win_conv_f32: unknown tile configuration"; return 1;
+  } else {
+    auto dispatch = [&](int c, const ConvArgs& a) -> cudaError_t {
+      cudaError_t e = cudaSuccess;
+      switch (c) {
+        case 0: { IM2WIN_DISPATCH(128, 128, 16) break; }
+        case 1: { IM2WIN_DISPATCH(64, 256, 16) break; }
+        case 2: { IM2WIN_DISPATCH(96, 128, 16) break; }
+        case 3: { IM2WIN_DISPATCH(128, 64, 16) break; }
+        case 4: { IM2WIN_DISPATCH4(64, 64, 16) break; }
+        case 5: { IM2WIN_DISPATCH4(128, 32, 16) break; }
+        default: { IM2WIN_DISPATCH4(32, 128, 16) break; }
+      }
+      return e;
+    };
+    // Tail split (library choice only): when the last wave of 8x8-micro-tile CTAs would leave
+    // most SMs idle, the full waves run as usual and the remaining GEMM columns go to a second
+    // launch of 4x4-micro-tile CTAs (4x the CTAs, so the tail spreads over every SM).  Each
+    // output is still computed by one thread over the whole K: same bits.
+    int tail_cfg = -1;
+    uint32_t n_main = 0;
+    if (auto_cfg && vec && stages > 1 && (cfg == 0 || cfg == 1 || cfg == 2)) {
+      static thread_local int sms_cache = 0;
+      if (!sms_cache) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms_cache, cudaDevAttrMultiProcessorCount, dev);
+        if (sms_cache <= 0) sms_cache = 148;
+      }
+      const int64_t bm = kBM[cfg], bn = cfg == 1 ? 256 : 128;
+      const int64_t m_t = (c_out + bm - 1) / bm, n_t = (n_gemm + bn - 1) / bn;
+      const int64_t ctas = m_t * n_t, slots = 2LL * sms_cache;
+      const int64_t full = ctas / slots * slots, tail = ctas - full;
+      const char* te = getenv("IM2WIN_SIMT_TAIL");
+      const double thr = te ? atof(te) : 0.75;
+      if (full >= slots && tail > 0 && static_cast<double>(tail) < thr * static_cast<double>(slots)) {
+        n_main = static_cast<uint32_t>(full / m_t * bn);
+        tail_cfg = cfg == 2 ? 6 : 4;
+      }
+    }
+    if (tail_cfg >= 0 && n_main > 0 && n_main < static_cast<uint32_t>(n_gemm)) {
+      ConvArgs am = a;
+      am.n_gemm = n_main;
+      e = dispatch(cfg, am);
+      if (e == cudaSuccess) {
+        ConvArgs at = a;
+        at.n_base = n_main;
+        e = dispatch(tail_cfg, at);
+      }
+    } else {
+      e = dispatch(cfg, a);
+    }
   }
 #undef IM2WIN_DISPATCH4
 #undef IM2WIN_DISPATCH
