@@ -24,6 +24,7 @@
 //   * register micro-kernel: each thread owns an 8x8 tile split into two 4x4
 //     quadrants so fragments are 128-bit shared loads ("vectorized load").
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -520,14 +521,16 @@ using im2win::ConvArgs;
 // Returns the configuration index chosen for (M, n_gemm); exposed for tests/bench.
 extern "C" int im2win_simt_pick(int M, long long n_gemm, int K) {
   (void)K;
-  // Measured (tools/tile_sweep.py, N=128): the 64x256 8x8 tile is the fastest wherever its
-  // grid fills the GPU; 96-channel layers use 96x128.  When the last wave of 2 CTAs/SM x 148
-  // SMs would leave the GPU under 75% busy, 4x4 micro-tiles (4x the threads) win.
+  // Measured (tools/tile_sweep.py, tools/simt_variants.py, N=128): the 64x256 8x8 tile is the
+  // fastest wherever its grid fills the GPU; 96-channel layers use 96x128.  A partial last
+  // wave is handled by the tail split in im2win_launch_conv_simt (conv6: 25.1 -> 26.9 TF over
+  // all-4x4 tiles); only a grid under one wave that would leave the GPU under 75% busy takes
+  // 4x4 micro-tiles (4x the threads): conv12 21.5 vs 17.6 TF.
   const long long slots = 148LL * 2;
   const bool m96 = M % 64 != 0 && M % 96 == 0;
   const long long ctas = m96 ? (M / 96) * ((n_gemm + 127) / 128) : ((M + 63) / 64) * ((n_gemm + 255) / 256);
-  const long long waves = (ctas + slots - 1) / slots;
-  if (static_cast<double>(ctas) / static_cast<double>(waves * slots) < 0.75) return m96 ? 6 : 4;
+  static const double below = getenv("IM2WIN_SIMT_MT4_BELOW") ? atof(getenv("IM2WIN_SIMT_MT4_BELOW")) : 0.75;
+  if (ctas < slots && static_cast<double>(ctas) / static_cast<double>(slots) < below) return m96 ? 6 : 4;
   return m96 ? 2 : 1;
 }
 

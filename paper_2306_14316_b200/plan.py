@@ -125,8 +125,9 @@ def simt_tile_for(dims: GemmDims) -> int:
     slots = 148 * 2
     m96 = dims.m % 64 != 0 and dims.m % 96 == 0
     ctas = (dims.m // 96) * -(-dims.n // 128) if m96 else -(-dims.m // 64) * -(-dims.n // 256)
-    waves = -(-ctas // slots)
-    if ctas / (waves * slots) < 0.75:
+    # a partial last wave is split off to 4x4 tiles by the launcher; only a grid under one
+    # wave that leaves the GPU under 75% busy runs on 4x4 tiles throughout
+    if ctas < slots and ctas / slots < 0.75:
         return 6 if m96 else 4
     return 2 if m96 else 1
 

@@ -101,11 +101,11 @@ def test_config1_checksum(layer_goldens):
 
 
 @pytest.mark.parametrize("name,batch", [("conv1", 128), ("conv7", 128), ("conv9", 128), ("conv12", 128),
-                                        ("conv4", 64), ("conv5", 128), ("conv10", 128)])
+                                        ("conv4", 64), ("conv5", 128), ("conv6", 128), ("conv10", 128)])
 def test_large_batch_sampled_images(name, batch):
     """Full-size runs: images are independent (reference.py:78-90), so sampled
     images checked against the oracle give the bits of the whole batch.  conv5/conv10
-    at N=128 take the SIMT tail split (the last images come from the 4x4-tile launch)."""
+    and conv6 at N=128 take the SIMT tail split (the last images come from the 4x4-tile launch)."""
     cfg = replace(BENCHMARKS[name], batch=batch, seed=7)
     g = torch.Generator(device="cpu").manual_seed(7)
     inp = torch.randn((batch, cfg.c_in, cfg.h_in, cfg.w_in), generator=g)
