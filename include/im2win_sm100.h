@@ -198,6 +198,10 @@ const char* im2win_last_error(void);
  * launched (which of the tile/kernel variants the library selected). */
 const char* im2win_last_kernel(void);
 
+/* Conv kernel launches made by this library so far (all threads; a layer may take two:
+ * the SIMT tail split).  bench.py counts the launches of its timed region with it. */
+int64_t im2win_conv_launch_count(void);
+
 /* ABI version of this library (major*100 + minor). */
 int32_t im2win_abi_version(void);
 

@@ -31,6 +31,7 @@ EXPORTED_SYMBOLS = (
     "im2win_conv_f32",
     "im2win_last_error",
     "im2win_last_kernel",
+    "im2win_conv_launch_count",
     "im2win_abi_version",
     "im2win_bench_fp32_peak",
     "im2win_transform_cl",
@@ -93,6 +94,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         lib.im2win_last_error.restype = ctypes.c_char_p
         lib.im2win_last_kernel.argtypes = []
         lib.im2win_last_kernel.restype = ctypes.c_char_p
+        lib.im2win_conv_launch_count.argtypes = []
+        lib.im2win_conv_launch_count.restype = ctypes.c_int64
         lib.im2win_abi_version.argtypes = []
         lib.im2win_abi_version.restype = ctypes.c_int32
         lib.im2win_bench_fp32_peak.argtypes = [vp, i32, i32, i32, vp]

@@ -1,3 +1,4 @@
+#include <atomic>
 // extern "C" boundary of libim2win_sm100.so (declared in include/im2win_sm100.h).
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -52,13 +53,20 @@ static int bind_device_of(const void* ptr) {
 int im2win_set_error(int code, const char* msg) { return fail(code, msg); }
 
 static thread_local const char* g_last_kernel = "";
-void im2win_note_kernel(const char* name) { g_last_kernel = name; }
+static std::atomic<long long> g_conv_launches{0};
+// every conv kernel launch site reports its kernel here (once per launch)
+void im2win_note_kernel(const char* name) {
+  g_last_kernel = name;
+  g_conv_launches.fetch_add(1, std::memory_order_relaxed);
+}
 
 extern "C" {
 
 const char* im2win_last_error(void) { return g_last_error; }
 
 const char* im2win_last_kernel(void) { return g_last_kernel; }
+
+int64_t im2win_conv_launch_count(void) { return g_conv_launches.load(std::memory_order_relaxed); }
 
 int32_t im2win_abi_version(void) { return 100; }
 

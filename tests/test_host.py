@@ -109,7 +109,7 @@ def test_fixture_roundtrip(tmp_path):
 
 def test_c_abi_library_exports_every_header_symbol():
     header = (ROOT / "include" / "im2win_sm100.h").read_text()
-    declared = set(re.findall(r"^\s*(?:int|size_t|const char\*|int32_t)\s+(im2win_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|size_t|const char\*|int32_t|int64_t)\s+(im2win_\w+)\s*\(", header, re.M))
     assert declared == set(_lib.EXPORTED_SYMBOLS)
     lib = _lib.load()
     for sym in declared:
