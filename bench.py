@@ -132,6 +132,8 @@ def load_traffic(names, batch: int, variant: str):
     alg = [d["layers"][n]["conv_algorithmic_bytes"] for n in names]
     return {"source": str(p.relative_to(ROOT)), "capture": d.get("capture"),
             "conv_bytes_per_launch": sum(conv) / len(conv),
+            "per_launch_note": "per layer conv call (mean over the 12 layers); a tail-split layer's two "
+                               "kernel launches count as one call",
             "conv_algorithmic_bytes_per_launch": sum(alg) / len(alg),
             "transform_bytes_per_launch": sum(xf) / len(xf),
             "per_layer": {n: d["layers"][n] for n in names}}

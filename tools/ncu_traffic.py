@@ -36,17 +36,25 @@ def val(r, i, table):
 
 launches = [(r[ki], val(r, rd, scale) + val(r, wr, scale), val(r, dur, tscale)) for r in data]
 names = list(BENCHMARKS)
-assert len(launches) == 2 * len(names), f"expected {2 * len(names)} launches, got {len(launches)}"
+# group per layer: one transform launch, then one or two conv launches (the SIMT tail split)
+groups = []
+for k, b, t in launches:
+    if "transform" in k:
+        groups.append({"bt": b, "tt": t, "bc": 0.0, "tc": 0.0, "nc": 0})
+    else:
+        assert "conv_simt" in k and groups, k
+        groups[-1]["bc"] += b
+        groups[-1]["tc"] += t
+        groups[-1]["nc"] += 1
+assert len(groups) == len(names), f"expected {len(names)} layers, got {len(groups)}"
 out = {"capture": "ncu --set full --clock-control none -k regex:'conv_simt|im2win_transform_pipe' "
                   f"python tools/run_all_layers.py --batch {batch} --variant {variant}",
        "batch": batch, "variant": variant, "layers": {}}
-for i, name in enumerate(names):
+for name, g in zip(names, groups):
     cfg = replace(BENCHMARKS[name], batch=batch)
-    (kt, bt, tt), (kc, bc, tc) = launches[2 * i], launches[2 * i + 1]
-    assert "transform" in kt and "conv_simt" in kc, (kt, kc)
-    out["layers"][name] = {"transform_dram_bytes": bt, "transform_algorithmic_bytes": cfg.transform_bytes(),
-                           "conv_dram_bytes": bc, "conv_algorithmic_bytes": cfg.conv_bytes(),
-                           "transform_ncu_s": tt, "conv_ncu_s": tc}
-    print(f"{name:7s} transform {bt / 1e6:9.1f} MB (alg {cfg.transform_bytes() / 1e6:9.1f})  "
-          f"conv {bc / 1e6:9.1f} MB (alg {cfg.conv_bytes() / 1e6:9.1f})")
+    out["layers"][name] = {"transform_dram_bytes": g["bt"], "transform_algorithmic_bytes": cfg.transform_bytes(),
+                           "conv_dram_bytes": g["bc"], "conv_algorithmic_bytes": cfg.conv_bytes(),
+                           "conv_launches": g["nc"], "transform_ncu_s": g["tt"], "conv_ncu_s": g["tc"]}
+    print(f"{name:7s} transform {g['bt'] / 1e6:9.1f} MB (alg {cfg.transform_bytes() / 1e6:9.1f})  "
+          f"conv {g['bc'] / 1e6:9.1f} MB (alg {cfg.conv_bytes() / 1e6:9.1f}) in {g['nc']} launch(es)")
 Path(dst).write_text(json.dumps(out, indent=1) + "\n")
