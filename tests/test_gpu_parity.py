@@ -451,8 +451,9 @@ def test_host_batch_api_order_and_bits():
 @pytest.mark.parametrize("variant", pkg.VARIANTS)
 def test_captured_conv_replays_bitwise(variant):
     """CapturedConv (CUDA-graph replay) equals conv_im2win_opt bit for bit, for new inputs and
-    a new filter on every replay, including a padded geometry."""
-    for name, pad in (("conv10", 0), ("conv9", 1)):
+    a new filter on every replay, including a padded geometry and a few-channel layer (conv2:
+    the direct TC kernel for TF32/BF16)."""
+    for name, pad in (("conv10", 0), ("conv9", 1), ("conv2", 0)):
         cfg = replace(BENCHMARKS[name], batch=3)
         params = pkg.ConvParams(cfg.c_in, cfg.c_out, cfg.h_f, cfg.w_f, cfg.stride, pad=pad)
         cap = pkg.CapturedConv((3, cfg.c_in, cfg.h_in, cfg.w_in), params, variant=variant)
