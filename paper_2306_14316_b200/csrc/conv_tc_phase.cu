@@ -352,8 +352,9 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
   if (mode == 0) return 0;
   // measured (tools/tc_kernels.py, N=128): stride 2 (conv4, Co=64) 1.57x over the generic fused
   // kernel; stride 1 with Co=64 (conv9, 4 tiles per item) 1.09x over the window-shift kernel;
-  // stride 1 with Co=128 (conv8, conv10): the shift kernel (conv_tc_shift.cu) is faster
-  if (mode == 1 && stride == 1 && c_out > 64) return 0;
+  // stride 1 with Co=128: the shift kernel (conv_tc_shift.cu) is faster for BF16 (conv8 868 vs 829
+  // TF) and for small outputs (conv10); TF32 on wide outputs prefers the phase kernel (conv8 528 vs 493)
+  if (mode == 1 && stride == 1 && c_out > 64 && (bf16 || (w - w_f + 1) < 64)) return 0;
   if (stride < 1 || stride > 2 || (w_f != 3 && w_f != 5 && w_f != 7) || c_out > 128) return 0;
   const int bk = bf16 ? 64 : 32;
   if (c_pad < 32) return 0;
