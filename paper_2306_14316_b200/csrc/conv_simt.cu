@@ -43,6 +43,9 @@
 #ifndef IM2WIN_SIMT_SMALLK_UNROLL
 #define IM2WIN_SIMT_SMALLK_UNROLL 4
 #endif
+#ifndef IM2WIN_SIMT_MINB192
+#define IM2WIN_SIMT_MINB192 2  // resident CTAs asked of the 192-thread 96x128 tile (register cap)
+#endif
 #ifndef IM2WIN_SIMT_INTERLEAVE
 #define IM2WIN_SIMT_INTERLEAVE 1
 #endif
@@ -107,7 +110,7 @@ IM2WIN_DEVICE float mac(float acc, float a, float b) {
 // The gather of slab kt+STAGES-1 is issued in BK/4 parts interleaved with the
 // compute of slab kt, so the 4-byte async copies do not arrive as one burst.
 template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC, int MT, bool SD>
-__global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? 2 : ((BM / MT) * (BN / MT) >= 512 ? 1 : 3))
+__global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? ((BM / MT) * (BN / MT) <= 192 ? IM2WIN_SIMT_MINB192 : 2) : ((BM / MT) * (BN / MT) >= 512 ? 1 : 3))
     conv_simt_kernel(const ConvArgs a) {
   constexpr int NT = (BM / MT) * (BN / MT);
   constexpr int TXN = BN / MT;                // threads along n
