@@ -573,11 +573,10 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
   using namespace im2win::tc;
   const int64_t cp = im2win_nhwc_channel_pitch(c_in, bf16);  // channel pitch of x_cl
   const int64_t h_out = (h - h_f) / stride + 1, w_out = (w - w_f) / stride + 1;
-  const int N = c_out <= 64 ? 64 : c_out <= 96 ? 96 : c_out <= 128 ? 128 : 256;
+  int N = c_out <= 64 ? 64 : c_out <= 96 ? 96 : c_out <= 128 ? 128 : 256;
   const int bk = bf16 ? 64 : 32;
   const int64_t Kfh = (w_f * cp + bk - 1) / bk * bk;
   const int64_t Kp = Kfh * h_f;
-  const int64_t Mp = (c_out + N - 1) / N * N;
   FusedArgs a{};
   a.out = out;
   a.n_img = static_cast<uint32_t>(n);
@@ -598,6 +597,24 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
   a.ow_tiles = (a.w_out + a.box_w - 1) / a.box_w;
   a.oh_tiles = (a.h_out + a.box_h - 1) / a.box_h;
   a.n_tiles = (a.n_img + a.box_n - 1) / a.box_n;
+  {
+    // few pixel tiles (conv12 at N=128: 26 tiles of 125 pixels): narrower Co tiles put more
+    // CTAs on the SMs (each re-reads its A tiles from L2)
+    static thread_local int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (sms <= 0) sms = 148;
+    }
+    const char* ne = getenv("IM2WIN_FUSED_NARROW");
+    const uint64_t ptiles = static_cast<uint64_t>(a.ow_tiles) * a.oh_tiles * a.n_tiles;
+    // (not below 128: a 128x64 UMMA is shared-memory bound -- conv12 at N = 64 measured 224 vs 274 TF)
+    if (!(ne && atoi(ne) == 0) && N == 256 &&
+        ptiles * static_cast<uint64_t>((c_out + N - 1) / N) < static_cast<uint64_t>(sms))
+      N = 128;
+  }
+  const int64_t Mp = (c_out + N - 1) / N * N;
   a.fh_slabs = static_cast<uint32_t>(Kfh / bk);
   a.k_slabs = a.fh_slabs * h_f;
   {
