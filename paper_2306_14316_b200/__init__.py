@@ -5,7 +5,7 @@ for the hot path: `im2win`, `Im2winTensor`, `conv_im2win_opt`,
 `compute_from_windows_opt`, `TilePlan`, `default_plan`, `GemmDims`,
 `ConvParams`, `Tensor4`, `output_dims`, `max_rel_diff`, `footprint_elems`,
 `im2win_gather`, the error types and the benchmark harness (`run_bench`,
-`run_ablation`, `report_csv`, `footprint_report`, `BenchRecord`, `ALGORITHMS`).
+`run_ablation`, `search_plan`, `report_csv`, `footprint_report`, `BenchRecord`, `ALGORITHMS`).
 The reference's CPU baselines (`conv_direct`, `conv_im2col_gemm`,
 `conv_implicit_gemm`, `gemm`, `im2col`, `Mat2`) and its worker pool are not
 rebuilt: on the GPU the baselines are cuDNN and im2col+cuBLAS (harness
@@ -37,7 +37,15 @@ from .kernels import (
 )
 from .workloads import BENCHMARKS, BenchConfig, make_inputs
 from .fixture_io import read_tensor, write_tensor
-from .harness import ALGORITHMS, BenchRecord, footprint_report, report_csv, run_ablation, run_bench
+from .harness import (
+    ALGORITHMS,
+    BenchRecord,
+    footprint_report,
+    report_csv,
+    run_ablation,
+    run_bench,
+    search_plan,
+)
 
 __version__ = "0.1.0"
 
@@ -50,6 +58,7 @@ __all__ = [
     "report_csv",
     "run_ablation",
     "run_bench",
+    "search_plan",
     "BENCHMARKS",
     "BenchConfig",
     "CapturedConv",

@@ -117,6 +117,18 @@ int64_t pick_chunk(int64_t n, int64_t chunk) {
   return std::max<int64_t>(1, (n + 3) / 4);
 }
 
+// Restores the calling thread's current device on scope exit: the host entry points bind
+// the workspace's device, and the caller's later default-device work must not move with it.
+struct DeviceGuard {
+  int saved = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&saved) != cudaSuccess) saved = -1;
+  }
+  ~DeviceGuard() {
+    if (saved >= 0) cudaSetDevice(saved);
+  }
+};
+
 }  // namespace
 
 extern "C" {
@@ -154,6 +166,7 @@ static int host_conv(const float* host_in, const float* host_flt, float* host_ou
     return im2win_set_error(1, "im2win_conv_host_f32: workspace is not device memory");
   const int dev = attr.device;
   if (dev < 0 || dev >= kMaxDev) return im2win_set_error(1, "im2win_conv_host_f32: device index out of range");
+  DeviceGuard guard;
   cudaSetDevice(dev);
   DevPipe& P = g_pipes[dev];
   std::lock_guard<std::mutex> lock(P.mu);
@@ -241,6 +254,13 @@ static int host_conv(const float* host_in, const float* host_flt, float* host_ou
                     cudaMemcpyDeviceToHost, P.d2h);
     cudaEventRecord(P.out_done[s], P.d2h);
   }
+  if (rc) {
+    // an entry point failed mid-loop: chunks already queued may still be reading or writing
+    // the workspace; drain all three streams so the caller can free or reuse it at once
+    cudaStreamSynchronize(P.h2d);
+    cudaStreamSynchronize(P.comp);
+    cudaStreamSynchronize(P.d2h);
+  }
   if (ticket) {
     // non-blocking: completion is ticket-tracked; the caller's stream is not made to wait,
     // so the next submission's uploads overlap this one's downloads
@@ -294,6 +314,7 @@ int im2win_conv_host_wait(int64_t ticket) {
     // completes after t, so waiting on it is still correct (just later)
     ev = P.done[t % kRing];
   }
+  DeviceGuard guard;
   cudaSetDevice(dev);
   cudaError_t e = cudaEventSynchronize(ev);
   return e == cudaSuccess ? 0 : im2win_set_error(2, cudaGetErrorString(e));

@@ -29,8 +29,8 @@ from .kernels import (
     nhwc_pitch,
 )
 from .layouts import im2win_into
-from .plan import TilePlan, gpu_plan
-from .workloads import BENCHMARKS, BenchConfig
+from .plan import SIMT_K_SLAB, SIMT_TILES, SIMT_TILES_MT4, TilePlan, gpu_plan
+from .workloads import BENCHMARKS, BenchConfig, make_inputs
 
 ALGORITHMS = ("im2win-opt", "im2win-basic", "im2win-fma", "im2win-tf32", "im2win-bf16", "cudnn", "im2col-cublas")
 ABLATION_VARIANTS = ("full", "-prefetch-double-buffer", "-vectorized-load", "-micro-kernel")
@@ -91,10 +91,10 @@ def _check_memory_budget(cfg: BenchConfig, algorithm: str, device) -> None:
 
 
 def _make_device_inputs(cfg: BenchConfig, device) -> tuple[torch.Tensor, torch.Tensor]:
-    g = torch.Generator(device=device).manual_seed(cfg.seed)
-    x = torch.randn((cfg.batch, cfg.c_in, cfg.h_in, cfg.w_in), device=device, generator=g)
-    f = torch.randn((cfg.c_out, cfg.c_in, cfg.h_f, cfg.w_f), device=device, generator=g)
-    return x, f
+    """The reference's seeded operands (numpy PCG64, bench.py:152-159) uploaded to the device,
+    so a record's checksum equals the reference's record for the same config."""
+    inp, flt = make_inputs(cfg)
+    return torch.from_numpy(inp).to(device), torch.from_numpy(flt).to(device)
 
 
 class _IeeeFp32:
@@ -159,65 +159,137 @@ def _stages(cfg: BenchConfig, algorithm: str, x, f, plan: TilePlan | None):
     raise ValueError(f"unknown algorithm {algorithm!r}, expected one of {ALGORITHMS}")
 
 
-def run_bench(cfg: BenchConfig, algorithm: str = "im2win-opt", repeats: int = 10, plan: TilePlan | None = None,
-              variant: str = "-", device=None) -> BenchRecord:
-    """Warm up once, run `repeats` times, report the fastest run (bench.py:226-266)."""
+# The reference's CPU baselines (bench.py:32) map onto their GPU counterparts on this device:
+# its per-image im2col + GEMM becomes im2col + cuBLAS, its direct and implicit-GEMM loops
+# become cuDNN (which picks implicit GEMM / Winograd / FFT itself).
+REFERENCE_ALIASES = {"im2col-gemm": "im2col-cublas", "direct": "cudnn", "implicit-gemm": "cudnn"}
+
+
+def run_bench(cfg: BenchConfig, variant: str = "-", *, device=None) -> BenchRecord:
+    """Warm up once, run `cfg.repeats` times, report the fastest run (bench.py:226-266).
+
+    Same call as the reference: `cfg.algorithm`, `cfg.repeats` and `cfg.plan` come from
+    the config (bench.py:43-59), `variant` is the record's label.  Extras are keyword-only.
+    """
+    algorithm = REFERENCE_ALIASES.get(cfg.algorithm, cfg.algorithm)
     if algorithm not in ALGORITHMS:
-        raise ValueError(f"unknown algorithm {algorithm!r}, expected one of {ALGORITHMS}")
-    if repeats < 1:
+        raise ValueError(f"unknown algorithm {cfg.algorithm!r}, expected one of {ALGORITHMS}")
+    if cfg.repeats < 1:
         raise ValueError("repeats must be >= 1")
+    repeats, plan = cfg.repeats, cfg.plan
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     _check_memory_budget(cfg, algorithm, dev)
     prev_tf32 = torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32
     torch.backends.cudnn.allow_tf32 = torch.backends.cuda.matmul.allow_tf32 = False
     try:
-        x, f = _make_device_inputs(cfg, dev)
-        torch.cuda.synchronize(dev)
-        base = torch.cuda.memory_allocated(dev)
-        torch.cuda.reset_peak_memory_stats(dev)
-        tr, cv, out = _stages(cfg, algorithm, x, f, plan)
-        tr()
-        cv()
-        torch.cuda.synchronize(dev)
-        peak = torch.cuda.max_memory_allocated(dev) - base
-        stream = torch.cuda.current_stream(dev)
-        best, totals = None, []
-        for _ in range(repeats):
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            e[0].record(stream)
-            tr()
-            e[1].record(stream)
-            cv()
-            e[2].record(stream)
+        with torch.cuda.device(dev):
+            x, f = _make_device_inputs(cfg, dev)
             torch.cuda.synchronize(dev)
-            t_tr, t_cv = e[0].elapsed_time(e[1]) * 1e-3, e[1].elapsed_time(e[2]) * 1e-3
-            totals.append(t_tr + t_cv)
-            if best is None or totals[-1] < best[0]:
-                best = (totals[-1], t_tr, t_cv)
-        checksum = checksum_tensor(out)
+            base = torch.cuda.memory_allocated(dev)
+            torch.cuda.reset_peak_memory_stats(dev)
+            tr, cv, out = _stages(cfg, algorithm, x, f, plan)
+            tr()
+            cv()
+            torch.cuda.synchronize(dev)
+            peak = torch.cuda.max_memory_allocated(dev) - base
+            stream = torch.cuda.current_stream(dev)
+            best, totals = None, []
+            for _ in range(repeats):
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                e[0].record(stream)
+                tr()
+                e[1].record(stream)
+                cv()
+                e[2].record(stream)
+                torch.cuda.synchronize(dev)
+                t_tr, t_cv = e[0].elapsed_time(e[1]) * 1e-3, e[1].elapsed_time(e[2]) * 1e-3
+                totals.append(t_tr + t_cv)
+                if best is None or totals[-1] < best[0]:
+                    best = (totals[-1], t_tr, t_cv)
+            checksum = checksum_tensor(out)
     finally:
         torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32 = prev_tf32
     total, t_tr, t_cv = best
     h_out, w_out = cfg.out_dims
     col, win = cfg.elems("im2col"), cfg.elems("im2win")
     return BenchRecord(
-        name=cfg.name, algorithm=algorithm, variant=variant, batch=cfg.batch, repeats=repeats, h_out=h_out,
+        name=cfg.name, algorithm=cfg.algorithm, variant=variant, batch=cfg.batch, repeats=repeats, h_out=h_out,
         w_out=w_out, flops=cfg.flops, transform_s=t_tr, compute_s=t_cv, total_s=total,
         tflops=cfg.flops / total / 1e12, raw_elems=cfg.elems("raw"), im2col_elems=col, im2win_elems=win,
         footprint_reduction_pct=100.0 * (1.0 - win / col), checksum=checksum, device=torch.cuda.get_device_name(dev),
         peak_mem_bytes=int(peak), timing_spread_s=max(totals) - min(totals))
 
 
-def run_ablation(cfg: BenchConfig, repeats: int = 10, device=None) -> list[BenchRecord]:
-    """Full tiled kernel, then each optimisation removed one at a time (bench.py:269-282, paper Fig. 4)."""
-    base = gpu_plan(cfg.gemm_dims())
+def run_ablation(cfg: BenchConfig, *, device=None) -> list[BenchRecord]:
+    """Full tiled kernel, then each optimisation removed one at a time (bench.py:269-282, paper Fig. 4).
+
+    The base plan is `cfg.plan` when given, else the tile the GPU library runs for the shape.
+    """
+    base = cfg.plan if cfg.plan is not None else gpu_plan(cfg.gemm_dims())
     plans = {
         "full": base,
         "-prefetch-double-buffer": base.with_toggles(prefetch_double_buffer=False),
         "-vectorized-load": base.with_toggles(vectorized_load=False),
         "-micro-kernel": base.with_toggles(micro_kernel=False),
     }
-    return [run_bench(cfg, "im2win-opt", repeats, plan, label, device) for label, plan in plans.items()]
+    return [run_bench(replace(cfg, algorithm="im2win-opt", plan=plan), label, device=device)
+            for label, plan in plans.items()]
+
+
+# The reference searches (m_b, n_b, k_b) over a CPU grid (bench.py:334-339).  On the GPU the
+# searchable space is the set of CTA tiles compiled into the FP32 kernel (plan.SIMT_TILES*),
+# each with its own register micro-tile and the 16-deep K slab.
+DEFAULT_SEARCH_GRID = tuple((m_b, n_b, SIMT_K_SLAB) for m_b, n_b in SIMT_TILES + SIMT_TILES_MT4)
+
+
+def _compiled_plan(m_b: int, n_b: int, k_b: int) -> TilePlan | None:
+    if k_b != SIMT_K_SLAB:
+        return None
+    if (m_b, n_b) in SIMT_TILES:
+        return TilePlan(m_b=m_b, n_b=n_b, k_b=k_b, m_t=8, n_t=8)
+    if (m_b, n_b) in SIMT_TILES_MT4:
+        return TilePlan(m_b=m_b, n_b=n_b, k_b=k_b, m_t=4, n_t=4)
+    return None
+
+
+def search_plan(cfg: BenchConfig, grid=DEFAULT_SEARCH_GRID, repeats: int = 1, *,
+                device=None) -> list[tuple[TilePlan, float]]:
+    """Grid search over block extents; returns (plan, seconds) sorted fastest-first (bench.py:342-364).
+
+    Grid entries that do not name a compiled GPU tile are skipped, as the reference skips
+    entries whose micro-tile does not divide the block.  Each plan is warmed up once and
+    timed `repeats` times with CUDA events on the current stream (best run kept).
+    """
+    if repeats < 1:
+        raise ValueError("repeats must be >= 1")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    p = cfg.params
+    results = []
+    with torch.cuda.device(dev):
+        x, f = _make_device_inputs(cfg, dev)
+        h_out, w_out = cfg.out_dims
+        win = torch.empty((cfg.batch, cfg.c_in, h_out, cfg.h_f * cfg.w_eff), device=dev)
+        out = torch.empty((cfg.batch, cfg.c_out, h_out, w_out), device=dev)
+        im2win_into(x, win, p)
+        stream = torch.cuda.current_stream(dev)
+        seen = set()
+        for m_b, n_b, k_b in grid:
+            plan = _compiled_plan(m_b, n_b, k_b)
+            if plan is None or plan in seen:
+                continue
+            seen.add(plan)
+            conv_windows_into(win, f, out, p, cfg.w_eff, plan)  # warm-up
+            best = float("inf")
+            for _ in range(repeats):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                conv_windows_into(win, f, out, p, cfg.w_eff, plan)
+                b.record(stream)
+                torch.cuda.synchronize(dev)
+                best = min(best, a.elapsed_time(b) * 1e-3)
+            results.append((plan, best))
+    results.sort(key=lambda pair: pair[1])
+    return results
 
 
 def _fmt(value) -> str:

@@ -414,7 +414,9 @@ def conv_im2win_opt_host(inp, flt, params: ConvParams, plan: TilePlan | None = N
     args = (x.data_ptr(), f.data_ptr(), out.data_ptr(), n_img, c_in, h_in, w_in, params.c_out, params.h_f,
             params.w_f, params.stride, params.pad, cp, code, chunk_images)
     if wait:
-        ws = _workspace(dev, stream, nbytes)
+        # per call (torch's caching allocator recycles it): the chunk buffers can be GBs at large N,
+        # so they are not pinned in the module-level workspace cache the device entry points share
+        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
         _lib.check(lib.im2win_conv_host_f32(*args, ws.data_ptr(), ws.numel(), stream))
         return out
     import ctypes

@@ -40,11 +40,22 @@ def local_slice(t: torch.Tensor, world: int, rank: int) -> torch.Tensor:
     return t[lo:hi]
 
 
+def _staged(group, t: torch.Tensor) -> bool:
+    """gloo moves host memory: CUDA operands of a gloo group are staged through host copies
+    (ranks sharing one GPU in tests; NCCL groups move device memory directly)."""
+    return t.is_cuda and dist.get_backend(group) != "nccl"
+
+
 def broadcast_filter(flt: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
     """Replicate the filter from `src` to every rank (one NCCL broadcast)."""
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         flt = flt.contiguous()
-        dist.broadcast(flt, src=src, group=group)
+        if _staged(group, flt):
+            h = flt.cpu()
+            dist.broadcast(h, src=src, group=group)
+            flt.copy_(h)
+        else:
+            dist.broadcast(flt, src=src, group=group)
     return flt
 
 
@@ -62,12 +73,18 @@ def gather_batch(local: torch.Tensor, n_total: int, dst: int | None = 0, group=N
     if int(local.shape[0]) != hi - lo:
         raise ShapeError(f"rank {rank} holds {local.shape[0]} images, expected {hi - lo}")
     tail = tuple(int(d) for d in local.shape[1:])
+    home = local.device
+    if _staged(group, local):
+        local = local.cpu()
     padded = torch.zeros((per,) + tail, dtype=local.dtype, device=local.device)
     padded[: hi - lo] = local
     if dst is None:
         full = torch.empty((per * world,) + tail, dtype=local.dtype, device=local.device)
-        dist.all_gather_into_tensor(full, padded, group=group)
-        return full[:n_total]
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(full, padded, group=group)
+        else:
+            dist.all_gather(list(full.chunk(world)), padded, group=group)
+        return full[:n_total].to(home)
     if dist.get_backend(group) == "nccl":
         parts = [torch.empty_like(padded) for _ in range(world)] if rank == dst else None
         dist.gather(padded, gather_list=parts, dst=dst, group=group)
@@ -78,7 +95,7 @@ def gather_batch(local: torch.Tensor, n_total: int, dst: int | None = 0, group=N
             parts = None
     if rank != dst:
         return None
-    return torch.cat(parts, dim=0)[:n_total]
+    return torch.cat(parts, dim=0)[:n_total].to(home)
 
 
 def conv_im2win_opt_sharded(inp_local: torch.Tensor, flt: torch.Tensor, params, *, n_total: int | None = None,
@@ -97,7 +114,15 @@ def conv_im2win_opt_sharded(inp_local: torch.Tensor, flt: torch.Tensor, params, 
         def compute(x, f):
             return conv_im2win_opt(x, f, params, plan, variant=variant).data
 
-    out_local = compute(inp_local, flt)
+    if int(inp_local.shape[0]) == 0:
+        # a tail rank can own no images (shard_bounds: n=9, world=4 -> 3,3,3,0); it still
+        # joins the gather collective with an empty slice instead of calling the kernels
+        from .tensors import output_dims
+
+        h_out, w_out = output_dims(int(inp_local.shape[2]), int(inp_local.shape[3]), params)
+        out_local = torch.empty((0, params.c_out, h_out, w_out), dtype=torch.float32, device=inp_local.device)
+    else:
+        out_local = compute(inp_local, flt)
     if not gather:
         return out_local
     if n_total is None:

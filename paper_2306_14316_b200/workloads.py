@@ -1,7 +1,8 @@
 """The paper's twelve benchmark layers and seeded synthetic operands.
 
 Mirrors winconv `bench.py`: `BenchConfig` (/root/reference/pkg/src/winconv/bench.py:43-80),
-`BENCHMARKS` (:88-104), `make_inputs` (:152-159, numpy PCG64 standard normal,
+same fields and defaults
+(batch, repeats, algorithm, plan, seed), `BENCHMARKS` (:88-104), `make_inputs` (:152-159, numpy PCG64 standard normal,
 input drawn first then filter) and the FLOP formula (:70-74).  Operand
 generation stays on the host with numpy so that GPU outputs can be compared
 bit for bit against the reference's own outputs on identical inputs.
@@ -13,7 +14,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .plan import GemmDims
+from .plan import GemmDims, TilePlan
 from .tensors import ConvParams, output_dims
 from .layouts import footprint_elems
 
@@ -31,6 +32,9 @@ class BenchConfig:
     w_f: int
     stride: int
     batch: int = 2
+    repeats: int = 10
+    algorithm: str = "im2win-opt"
+    plan: TilePlan | None = None
     seed: int = 0
 
     @property

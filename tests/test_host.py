@@ -177,3 +177,28 @@ def test_harness_names_match_reference():
     assert harness.CSV_COLUMNS[:17] == ("name", "algorithm", "variant", "batch", "repeats", "h_o", "w_o", "flops",
                                         "transform_s", "compute_s", "total_s", "tflops", "raw_elems",
                                         "im2col_elems", "im2win_elems", "footprint_reduction_pct", "checksum")
+
+
+def test_bench_config_is_the_reference_dataclass():
+    """BenchConfig carries the reference's fields and defaults (bench.py:43-59), so
+    replace(BENCHMARKS[n], batch=N, repeats=R, algorithm=...) works unchanged."""
+    import dataclasses
+    import inspect
+
+    from paper_2306_14316_b200 import harness
+    from paper_2306_14316_b200.workloads import BENCHMARKS, BenchConfig
+
+    fields = [(f.name, f.default) for f in dataclasses.fields(BenchConfig)]
+    assert [n for n, _ in fields] == ["name", "c_in", "h_in", "w_in", "c_out", "h_f", "w_f", "stride", "batch",
+                                      "repeats", "algorithm", "plan", "seed"]
+    assert dict(fields)["repeats"] == 10 and dict(fields)["algorithm"] == "im2win-opt"
+    assert dict(fields)["plan"] is None and dict(fields)["batch"] == 2 and dict(fields)["seed"] == 0
+    cfg = dataclasses.replace(BENCHMARKS["conv9"], batch=8, repeats=3, algorithm="im2win-opt")
+    assert (cfg.batch, cfg.repeats, cfg.algorithm) == (8, 3, "im2win-opt")
+    sig = inspect.signature(harness.run_bench)
+    assert list(sig.parameters)[:2] == ["cfg", "variant"] and sig.parameters["variant"].default == "-"
+    assert sig.parameters["device"].kind is inspect.Parameter.KEYWORD_ONLY
+    assert list(inspect.signature(harness.search_plan).parameters)[:3] == ["cfg", "grid", "repeats"]
+    # the reference's CPU baselines resolve to their GPU counterparts
+    assert set(harness.REFERENCE_ALIASES) == {"direct", "im2col-gemm", "implicit-gemm"}
+    assert all(a in harness.ALGORITHMS for a in harness.REFERENCE_ALIASES.values())
