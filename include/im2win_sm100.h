@@ -132,6 +132,20 @@ int im2win_conv_fused(const void* x_nhwc, const float* flt, float* out, int64_t 
                       int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
                       int32_t variant, void* workspace, size_t workspace_bytes, void* stream);
 
+/* One call for the whole TF32/BF16 conv_im2win_opt (replaces the numba conv_im2win_opt,
+ * pkg/src/winconv/kernels/optimized.py:237-241, for the tensor-core variants): x is the
+ * NCHW float32 input; x_nhwc is caller-provided scratch of n*h*w*pitch elements
+ * (pitch = channel pitch of im2win_nchw_to_nhwc for the variant's dtype) that extra warps
+ * of the conv kernel fill while the tensor cores run, instead of a separate copy kernel
+ * before it.  Same results as im2win_nchw_to_nhwc + im2win_conv_fused, bit for bit. */
+size_t im2win_conv_fused_nchw_workspace_bytes(int64_t n, int64_t c_in, int64_t c_out, int32_t h_f,
+                                              int32_t w_f);
+
+int im2win_conv_fused_nchw(const float* x, void* x_nhwc, const float* flt, float* out, int64_t n,
+                           int64_t c_in, int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f,
+                           int32_t stride, int32_t variant, void* workspace, size_t workspace_bytes,
+                           void* stream);
+
 /* ---- Direct tensor-core path for few-channel inputs (extension) ----
  * For C <= 16 (the RGB input layers) producer warps build each output pixel's im2win
  * window (k = (c, fh, fw), C*Hf*Wf values) from an input patch staged in shared memory

@@ -41,6 +41,8 @@ EXPORTED_SYMBOLS = (
     "im2win_nchw_to_nhwc_padded",
     "im2win_conv_fused_workspace_bytes",
     "im2win_conv_fused",
+    "im2win_conv_fused_nchw_workspace_bytes",
+    "im2win_conv_fused_nchw",
     "im2win_conv_basic_f32",
     "im2win_conv_direct_supported",
     "im2win_conv_direct_preferred",
@@ -114,6 +116,11 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         lib.im2win_conv_fused_workspace_bytes.restype = sz
         lib.im2win_conv_fused.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32, i32, vp, sz, vp]
         lib.im2win_conv_fused.restype = ctypes.c_int
+        lib.im2win_conv_fused_nchw_workspace_bytes.argtypes = [i64, i64, i64, i32, i32]
+        lib.im2win_conv_fused_nchw_workspace_bytes.restype = sz
+        lib.im2win_conv_fused_nchw.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32, i32, vp, sz,
+                                               vp]
+        lib.im2win_conv_fused_nchw.restype = ctypes.c_int
         lib.im2win_conv_basic_f32.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i32, i32, i32, vp]
         lib.im2win_conv_basic_f32.restype = ctypes.c_int
         lib.im2win_conv_direct_supported.argtypes = [i64, i64, i64, i64, i64, i32, i32, i32, i32, i32]

@@ -199,7 +199,8 @@ int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c
 size_t im2win_tc_fused_workspace_bytes(int64_t c_in, int64_t c_out, int h_f, int w_f);
 int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n,
                                 int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride,
-                                int bf16, cudaStream_t stream, const char** err);
+                                int bf16, const float* feed_src, cudaStream_t stream, const char** err);
+size_t im2win_tc_fused_feed_workspace_bytes(int64_t n, int64_t c_in, int64_t c_out, int h_f, int w_f);
 
 extern "C" {
 
@@ -241,7 +242,32 @@ int im2win_conv_fused(const void* x_nhwc, const float* flt, float* out, int64_t 
   if (int rc = bind_device_of(out)) return rc;
   const char* err = nullptr;
   int rc = im2win_launch_conv_tc_fused(x_nhwc, flt, out, workspace, n, c_in, h, w, c_out, h_f, w_f, stride,
-                                       variant == IM2WIN_BF16, static_cast<cudaStream_t>(stream), &err);
+                                       variant == IM2WIN_BF16, nullptr, static_cast<cudaStream_t>(stream), &err);
+  return rc ? fail(rc, err) : 0;
+}
+
+size_t im2win_conv_fused_nchw_workspace_bytes(int64_t n, int64_t c_in, int64_t c_out, int32_t h_f, int32_t w_f) {
+  return im2win_tc_fused_feed_workspace_bytes(n, c_in, c_out, h_f, w_f);
+}
+
+int im2win_conv_fused_nchw(const float* x, void* x_nhwc, const float* flt, float* out, int64_t n, int64_t c_in,
+                           int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
+                           int32_t variant, void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_error[0] = '\0';
+  if (!x || !x_nhwc || !flt || !out || !workspace) return fail(1, "im2win_conv_fused_nchw: null pointer");
+  if (n < 1 || c_in < 1 || c_out < 1 || h < 1 || w < 1 || h_f < 1 || w_f < 1 || stride < 1)
+    return fail(1, "im2win_conv_fused_nchw: extents must be positive");
+  if (h_f > h || w_f > w) return fail(1, "im2win_conv_fused_nchw: filter larger than input");
+  if (variant != IM2WIN_TF32 && variant != IM2WIN_BF16)
+    return fail(1, "im2win_conv_fused_nchw: variant must be IM2WIN_TF32 or IM2WIN_BF16");
+  if (workspace_bytes < im2win_conv_fused_nchw_workspace_bytes(n, c_in, c_out, h_f, w_f))
+    return fail(1, "im2win_conv_fused_nchw: workspace too small");
+  if ((reinterpret_cast<uintptr_t>(x_nhwc) & 15) != 0 || (reinterpret_cast<uintptr_t>(workspace) & 15) != 0)
+    return fail(1, "im2win_conv_fused_nchw: x_nhwc and workspace must be 16-byte aligned");
+  if (int rc = bind_device_of(out)) return rc;
+  const char* err = nullptr;
+  int rc = im2win_launch_conv_tc_fused(x_nhwc, flt, out, workspace, n, c_in, h, w, c_out, h_f, w_f, stride,
+                                       variant == IM2WIN_BF16, x, static_cast<cudaStream_t>(stream), &err);
   return rc ? fail(rc, err) : 0;
 }
 

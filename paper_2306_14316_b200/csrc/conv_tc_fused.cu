@@ -211,9 +211,9 @@ struct TileWalk {
 // stays resident; only window tiles stream through the ring (small filters: the
 // 3-channel input layers, where staging the filter per tile doubles the TMA rows).
 template <bool BF16, int N, int STAGES, bool RB = false>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcThreadsFeed, 1)
     conv_tc_fused_kernel(const FusedArgs a, const __grid_constant__ CUtensorMap tmap_a,
-                         const __grid_constant__ CUtensorMap tmap_b) {
+                         const __grid_constant__ CUtensorMap tmap_b, const NhwcFeed feed) {
   constexpr uint32_t kABytes = kTileM * kRowBytes;
   constexpr uint32_t kBBytes = RB ? 0 : N * kRowBytes;
   constexpr uint32_t kStageBytes = kABytes + kBBytes;
@@ -272,6 +272,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (uint32_t ks = 0; ks < a.k_slabs; ++ks)
           tma_load_2d(smem_base + ks * N * kRowBytes, &tmap_b, &bres_bar, ks * kBK, 0);
       }
+      uint32_t conf_lo = 1, conf_hi = 0;
       for (TileWalk w(a.group); w.t < total_tiles; w.next()) {
         const uint32_t t = w.t;
         const uint32_t co_blk = t % a.co_tiles;
@@ -280,6 +281,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         pt /= a.ow_tiles;
         const uint32_t oh0 = (pt % a.oh_tiles) * a.box_h;
         const uint32_t n0 = (pt / a.oh_tiles) * a.box_n;
+        nhwc_feed_wait(feed, n0, n0 + a.box_n - 1, conf_lo, conf_hi);
         for (uint32_t ks = 0; ks < a.k_slabs; ++ks) {
           const uint32_t fh = ks / a.fh_slabs;
           const uint32_t j0 = (ks % a.fh_slabs) * kBK;
@@ -320,6 +322,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
+  } else if (warp >= 4 + kEpiWarps) {
+    if (feed.src)
+      nhwc_feed_run<BF16>(feed, lane, blockIdx.x * kFeedWarps + (warp - 4 - kEpiWarps), gridDim.x * kFeedWarps);
   } else if (warp >= 4) {
     // kEpiWarps epilogue warps: warp w reads TMEM lane quarter w % 4 and column half (w - 4) / 4
     const int quarter = warp % 4;
@@ -393,8 +398,8 @@ __global__ void pack_filter_fused_kernel(const float* __restrict__ flt, void* __
 
 template <bool BF16, int N, int STAGES, bool RB = false>
 static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64_t c_in, int64_t h, int64_t w,
-                        int32_t h_f, int32_t w_f, int32_t stride, int64_t Kp, int64_t Mp, cudaStream_t stream,
-                        const char** err) {
+                        int32_t h_f, int32_t w_f, int32_t stride, int64_t Kp, int64_t Mp, const NhwcFeed& feed,
+                        cudaStream_t stream, const char** err) {
   constexpr int kBK = BF16 ? 64 : 32;
   auto enc = get_encode_fn();
   if (!enc) {
@@ -457,8 +462,8 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
                               : "conv_tc_fused_kernel (generic TMA window boxes, filter resident, tf32)")
                      : (BF16 ? "conv_tc_fused_kernel (generic TMA window boxes, bf16)"
                              : "conv_tc_fused_kernel (generic TMA window boxes, tf32)"));
-  kern<<<grid, kTcThreads, smem, stream>>>(a, map_a, map_b);
-  e = cudaGetLastError();
+  e = launch_tc_kernel(kern, grid, smem, stream, feed.src != nullptr, a, map_a, map_b, feed);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
     return 2;
@@ -475,8 +480,48 @@ int64_t im2win_nhwc_channel_pitch(int64_t c, int bf16) {
   return (c + q - 1) / q * q;
 }
 
+namespace im2win {
+namespace tc {
+// The feed warps' code alone (no conv): tools/feed_ab.py measures its copy rate (IM2WIN_FEED_PROBE=1).
+template <bool BF16>
+__global__ void __launch_bounds__(32 * kFeedWarps) nhwc_feed_only_kernel(const NhwcFeed f) {
+  nhwc_feed_run<BF16>(f, threadIdx.x % 32, blockIdx.x * kFeedWarps + threadIdx.x / 32, gridDim.x * kFeedWarps);
+}
+}  // namespace tc
+}  // namespace im2win
+
 int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c, int64_t h, int64_t w, int bf16,
                                int pad, cudaStream_t stream, const char** err) {
+  if (pad == 0 && getenv("IM2WIN_FEED_PROBE") && atoi(getenv("IM2WIN_FEED_PROBE")) > 0) {
+    using namespace im2win::tc;
+    static uint32_t* counters = nullptr;
+    static int64_t cap = 0;
+    if (cap < n + 1) {
+      if (counters) cudaFree(counters);
+      cudaMalloc(&counters, (n + 1) * 4);
+      cap = n + 1;
+    }
+    NhwcFeed feed{};
+    feed.src = src;
+    feed.dst = dst;
+    feed.c_in = static_cast<uint32_t>(c);
+    feed.c_pad = static_cast<uint32_t>(im2win_nhwc_channel_pitch(c, bf16));
+    feed.hw = static_cast<uint32_t>(h * w);
+    feed.n_img = static_cast<uint32_t>(n);
+    const uint32_t pix = bf16 ? FeedShape<true>::kPix : FeedShape<false>::kPix;
+    const uint32_t grp = bf16 ? FeedShape<true>::G : FeedShape<false>::G;
+    feed.chunks = static_cast<uint32_t>((h * w + pix - 1) / pix);
+    feed.units_per_img = feed.chunks * ((feed.c_pad + grp - 1) / grp);
+    feed.ready = counters;
+    feed.next = counters + n;
+    cudaMemsetAsync(counters, 0, (n + 1) * 4, stream);
+    const int g = atoi(getenv("IM2WIN_FEED_PROBE"));  // CTAs of kFeedWarps warps
+    if (bf16) nhwc_feed_only_kernel<true><<<g, 32 * kFeedWarps, 0, stream>>>(feed);
+    else nhwc_feed_only_kernel<false><<<g, 32 * kFeedWarps, 0, stream>>>(feed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 2; }
+    return 0;
+  }
   using im2win::tc::PadMap;
   const int64_t hw = h * w;
   const int64_t cp = im2win_nhwc_channel_pitch(c, bf16);
@@ -559,18 +604,74 @@ size_t im2win_tc_fused_workspace_bytes(int64_t c_in, int64_t c_out, int h_f, int
   return static_cast<size_t>(Mp * std::max(Kfh, Kshift) * h_f) * 4 + 1024;
 }
 
+// The in-kernel feed's counters (n ready counters + 1 claim counter) follow the packed filter.
+uint32_t* im2win_tc_feed_counters(void* workspace, int64_t c_in, int64_t c_out, int h_f, int w_f) {
+  return reinterpret_cast<uint32_t*>(static_cast<char*>(workspace) +
+                                     im2win_tc_fused_workspace_bytes(c_in, c_out, h_f, w_f));
+}
+
+size_t im2win_tc_fused_feed_workspace_bytes(int64_t n, int64_t c_in, int64_t c_out, int h_f, int w_f) {
+  return im2win_tc_fused_workspace_bytes(c_in, c_out, h_f, w_f) + static_cast<size_t>(n + 1) * 4 + 256;
+}
+
 int im2win_try_conv_tc_shift(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n, int64_t c_in,
                              int64_t c_pad, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride, int bf16,
-                             double fused_util, cudaStream_t stream, const char** err);
+                             double fused_util, const im2win::tc::NhwcFeed& feed, cudaStream_t stream,
+                             const char** err);
 
 int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n, int64_t c_in,
                              int64_t c_pad, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride, int bf16,
-                             double fused_util, cudaStream_t stream, const char** err);
+                             double fused_util, const im2win::tc::NhwcFeed& feed, cudaStream_t stream,
+                             const char** err);
 
 int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n,
                                 int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride,
-                                int bf16, cudaStream_t stream, const char** err) {
+                                int bf16, const float* feed_src, cudaStream_t stream, const char** err) {
   using namespace im2win::tc;
+  // feed_src != nullptr: x_cl is scratch, produced from the NCHW input inside the conv kernel
+  // (counters at the end of the workspace, see im2win_tc_feed_counters)
+  NhwcFeed feed{};
+  if (feed_src) {
+    // In-kernel feed or a copy kernel first.  Measured (tools/feed_ab.py): the feed warps and the
+    // conv share the memory system, so overlap pays only where the conv's own traffic is light
+    // next to the input -- output/input elements r = (Co*Ho*Wo)/(C*H*W) <= 0.5 (strided layers:
+    // conv4 BF16 1.35 -> 0.97 ms, TF32 2.00 -> 1.82 ms at N=128); at r ~ 0.9 (conv9/10) it ties,
+    // and at r >= 1.4 (conv5/6/8) it loses up to 18%.  IM2WIN_FEED: 0 never, 1 auto, 2 always.
+    const char* fe = getenv("IM2WIN_FEED");
+    const int mode = fe ? atoi(fe) : 1;
+    const int64_t h_o = (h - h_f) / stride + 1, w_o = (w - w_f) / stride + 1;
+    const double r = static_cast<double>(c_out * h_o * w_o) / static_cast<double>(c_in * h * w);
+    if (mode == 0 || (mode == 1 && r > 0.5)) {
+      const int rc = im2win_launch_nchw_to_nhwc(feed_src, const_cast<void*>(x_cl), n, c_in, h, w, bf16, 0, stream, err);
+      if (rc) return rc;
+      feed_src = nullptr;
+    }
+  }
+  if (feed_src) {
+    const int64_t hw = h * w;
+    if (hw >= (1ll << 31) || n * ((hw + 63) / 64) * ((c_in + 7) / 8) >= (1ll << 32)) {
+      *err = "conv_tc_fused: extents exceed the feed's index range";
+      return 1;
+    }
+    feed.src = feed_src;
+    feed.dst = const_cast<void*>(x_cl);
+    feed.c_in = static_cast<uint32_t>(c_in);
+    feed.c_pad = static_cast<uint32_t>(im2win_nhwc_channel_pitch(c_in, bf16));
+    feed.hw = static_cast<uint32_t>(hw);
+    feed.n_img = static_cast<uint32_t>(n);
+    const uint32_t pix = bf16 ? FeedShape<true>::kPix : FeedShape<false>::kPix;
+    const uint32_t grp = bf16 ? FeedShape<true>::G : FeedShape<false>::G;
+    feed.chunks = static_cast<uint32_t>((hw + pix - 1) / pix);
+    feed.units_per_img = feed.chunks * ((feed.c_pad + grp - 1) / grp);
+    feed.ready = im2win_tc_feed_counters(workspace, c_in, c_out, h_f, w_f);
+    feed.next = feed.ready + n;
+    feed.nowait = getenv("IM2WIN_FEED_NOWAIT") && atoi(getenv("IM2WIN_FEED_NOWAIT")) ? 1u : 0u;
+    cudaError_t e = cudaMemsetAsync(feed.ready, 0, static_cast<size_t>(n + 1) * 4, stream);
+    if (e != cudaSuccess) {
+      *err = cudaGetErrorString(e);
+      return 2;
+    }
+  }
   const int64_t cp = im2win_nhwc_channel_pitch(c_in, bf16);  // channel pitch of x_cl
   const int64_t h_out = (h - h_f) / stride + 1, w_out = (w - w_f) / stride + 1;
   int N = c_out <= 64 ? 64 : c_out <= 96 ? 96 : c_out <= 128 ? 128 : 256;
@@ -621,14 +722,14 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
     // the phase kernel reuses each loaded A tile for every tap of a stride phase (any stride <= 2)
     const double util = static_cast<double>(a.box_w) * a.box_h * a.box_n / kTileM;
     const int rc = im2win_try_conv_tc_phase(x_cl, flt, out, workspace, n, c_in, cp, h, w, c_out, h_f, w_f, stride,
-                                            bf16, util, stream, err);
+                                            bf16, util, feed, stream, err);
     if (rc != 0) return rc > 0 ? 0 : -rc;
   }
   {
     // stride-1 layers: the window-shift kernel reuses each loaded A tile for all Wf taps
     const double util = static_cast<double>(a.box_w) * a.box_h * a.box_n / kTileM;
     const int rc = im2win_try_conv_tc_shift(x_cl, flt, out, workspace, n, c_in, cp, h, w, c_out, h_f, w_f, stride,
-                                            bf16, util, stream, err);
+                                            bf16, util, feed, stream, err);
     if (rc != 0) return rc > 0 ? 0 : -rc;
   }
   if (bf16)
@@ -642,9 +743,9 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
                                                              static_cast<int>(Mp), static_cast<int>(Kfh),
                                                              static_cast<int>(Kp));
 #define IM2WIN_FU(BF, NN, ST) \
-  return launch_fused<BF, NN, ST>(a, x_cl, workspace, cp, h, w, h_f, w_f, stride, Kp, Mp, stream, err)
+  return launch_fused<BF, NN, ST>(a, x_cl, workspace, cp, h, w, h_f, w_f, stride, Kp, Mp, feed, stream, err)
 #define IM2WIN_FU_RB(BF, NN) \
-  return launch_fused<BF, NN, 6, true>(a, x_cl, workspace, cp, h, w, h_f, w_f, stride, Kp, Mp, stream, err)
+  return launch_fused<BF, NN, 6, true>(a, x_cl, workspace, cp, h, w, h_f, w_f, stride, Kp, Mp, feed, stream, err)
   {
     // filter-resident mode: one Co tile whose whole packed filter fits beside 6 window stages
     const char* rb_env = getenv("IM2WIN_FUSED_RB");

@@ -39,9 +39,10 @@ struct PhaseArgs {
 constexpr int kPhRows = 136;  // 128 MMA rows + up to 8 rows of shift
 
 template <bool BF16, int N, int STAGES, int TAPS, int MT>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcThreadsFeed, 1)
     conv_tc_phase_kernel(const PhaseArgs a, const __grid_constant__ CUtensorMap tmap_a0,
-                         const __grid_constant__ CUtensorMap tmap_a1, const __grid_constant__ CUtensorMap tmap_b) {
+                         const __grid_constant__ CUtensorMap tmap_a1, const __grid_constant__ CUtensorMap tmap_b,
+                         const NhwcFeed feed) {
   constexpr uint32_t kATile = kPhRows * kRowBytes;  // 17 KB, multiple of 1024
   constexpr uint32_t kABytes = MT * kATile;
   constexpr uint32_t kBTap = N * kRowBytes;
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
+      uint32_t conf_lo = 1, conf_hi = 0;
       for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
         const uint32_t co_blk = t % a.co_tiles;
         const uint32_t pair = t / a.co_tiles;
@@ -112,6 +114,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           oh0[mt] = (pt % a.oh_tiles) * a.rows;
           n0[mt] = (pt / a.oh_tiles) * a.box_n;
         }
+        // pixel tiles are image-major: n0[0] is the lowest image, n0[MT-1] the highest
+        nhwc_feed_wait(feed, n0[0], n0[MT - 1] + a.box_n - 1, conf_lo, conf_hi);
         for (uint32_t ki = 0; ki < a.k_iters; ++ki) {
           const uint32_t c0 = (ki % a.c_slabs) * kBK;
           const uint32_t rem = ki / a.c_slabs;
@@ -171,6 +175,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
+  } else if (warp >= 4 + kEpiWarps) {
+    if (feed.src)
+      nhwc_feed_run<BF16>(feed, lane, blockIdx.x * kFeedWarps + (warp - 4 - kEpiWarps), gridDim.x * kFeedWarps);
   } else if (warp >= 4) {
     // kEpiWarps epilogue warps: warp w reads TMEM lane quarter w % 4 and column half (w - 4) / 4
     const int quarter = warp % 4;
@@ -249,7 +256,7 @@ inline double phase_tile(int64_t n, int64_t h_out, int64_t w_out, int64_t qmax, 
 
 template <bool BF16, int N, int STAGES, int TAPS, int MT>
 static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64_t c_pad, int64_t h, int64_t w,
-                        int64_t Mp, int64_t Kp, cudaStream_t stream, const char** err) {
+                        int64_t Mp, int64_t Kp, const NhwcFeed& feed, cudaStream_t stream, const char** err) {
   constexpr int kBK = BF16 ? 64 : 32;
   auto enc = get_encode_fn();
   if (!enc) {
@@ -304,7 +311,11 @@ static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64
   const uint64_t items = static_cast<uint64_t>(a.pairs) * a.co_tiles;
   const uint32_t grid = items < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(items) : static_cast<uint32_t>(sms);
   im2win_note_kernel(MT == 4 ? "conv_tc_phase_kernel (phase shift, 4 tiles/item)" : "conv_tc_phase_kernel (phase shift, 2 tiles/item)");
-  kern<<<grid, kTcThreads, smem, stream>>>(a, map_a[0], map_a[1], map_b);
+  e = launch_tc_kernel(kern, grid, smem, stream, feed.src != nullptr, a, map_a[0], map_a[1], map_b, feed);
+  if (e != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 2;
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
@@ -345,7 +356,8 @@ __global__ void pack_filter_phase_kernel(const float* __restrict__ flt, void* __
 // (a K-slab is one channel chunk of one tap), Co <= 128.
 int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n, int64_t c_in,
                              int64_t c_pad, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride, int bf16,
-                             double fused_util, cudaStream_t stream, const char** err) {
+                             double fused_util, const im2win::tc::NhwcFeed& feed, cudaStream_t stream,
+                             const char** err) {
   using namespace im2win::tc;
   const char* env = getenv("IM2WIN_PHASE");
   const int mode = env ? atoi(env) : 1;  // 0: off, 1: auto, 2: force where legal (tests)
@@ -404,7 +416,7 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
   int rc = 1;
   // stage = 2 x 17 KB of A + taps x N x 128 B of B; as many stages as fit in 227 KB
 #define IM2WIN_PH(BF, NN, ST, TP) \
-  rc = launch_phase<BF, NN, ST, TP, 2>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err)
+  rc = launch_phase<BF, NN, ST, TP, 2>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err)
 #define IM2WIN_PH_T(BF)                                        \
   switch (taps * 1000 + N) {                                   \
     case 2064: IM2WIN_PH(BF, 64, 4, 2); break;                 \
@@ -421,10 +433,10 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
     // stage = 4 x 17 KB of A + taps x 8 KB of B: two stages
 #define IM2WIN_PH4(BF)                                                                                   \
   switch (taps) {                                                                                        \
-    case 2: rc = launch_phase<BF, 64, 2, 2, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err); break; \
-    case 3: rc = launch_phase<BF, 64, 2, 3, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err); break; \
-    case 4: rc = launch_phase<BF, 64, 2, 4, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err); break; \
-    default: rc = launch_phase<BF, 64, 2, 5, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err); break; \
+    case 2: rc = launch_phase<BF, 64, 2, 2, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err); break; \
+    case 3: rc = launch_phase<BF, 64, 2, 3, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err); break; \
+    case 4: rc = launch_phase<BF, 64, 2, 4, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err); break; \
+    default: rc = launch_phase<BF, 64, 2, 5, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err); break; \
   }
     if (bf16) {
       IM2WIN_PH4(true)

@@ -37,9 +37,9 @@ IM2WIN_DEVICE uint64_t smem_desc_sw128_off(uint32_t addr) {
 }
 
 template <bool BF16, int N, int STAGES, int WF, bool RB>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcThreadsFeed, 1)
     conv_tc_shift_kernel(const ShiftArgs a, const __grid_constant__ CUtensorMap tmap_a,
-                         const __grid_constant__ CUtensorMap tmap_b) {
+                         const __grid_constant__ CUtensorMap tmap_b, const NhwcFeed feed) {
   constexpr uint32_t kABytes = kARows * kRowBytes;  // 17 KB (multiple of 1024)
   constexpr uint32_t kBBytes = RB ? 0 : WF * N * kRowBytes;  // RB: filter resident, not staged
   constexpr uint32_t kStageBytes = kABytes + kBBytes;
@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tma_load_2d(smem + (ks * WF + fw) * N * kRowBytes, &tmap_b, &bres_bar,
                         ((ks / a.c_slabs) * WF + fw) * a.c_slabs * kBK + (ks % a.c_slabs) * kBK, 0);
       }
+      uint32_t conf_lo = 1, conf_hi = 0;
       for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         const uint32_t co_blk = t % a.co_tiles;
         uint32_t pt = t / a.co_tiles;
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         pt /= a.ow_tiles;
         const uint32_t oh0 = (pt % a.oh_tiles) * a.rows;
         const uint32_t n0 = (pt / a.oh_tiles) * a.box_n;
+        nhwc_feed_wait(feed, n0, n0 + a.box_n - 1, conf_lo, conf_hi);
         for (uint32_t ks = 0; ks < a.k_slabs; ++ks) {
           const uint32_t fh = ks / a.c_slabs;
           const uint32_t c0 = (ks % a.c_slabs) * kBK;
@@ -165,6 +167,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
+  } else if (warp >= 4 + kEpiWarps) {
+    if (feed.src)
+      nhwc_feed_run<BF16>(feed, lane, blockIdx.x * kFeedWarps + (warp - 4 - kEpiWarps), gridDim.x * kFeedWarps);
   } else if (warp >= 4) {
     // kEpiWarps epilogue warps: warp w reads TMEM lane quarter w % 4 and column half (w - 4) / 4
     const int quarter = warp % 4;
@@ -259,7 +264,7 @@ inline double shift_tile(int64_t n, int64_t h_out, int64_t w_out, int w_f, Shift
 
 template <bool BF16, int N, int STAGES, int WF, bool RB>
 static int launch_shift(ShiftArgs a, const void* x_cl, const void* packed, int64_t c_in, int64_t h, int64_t w,
-                        int64_t Mp, int64_t Kp, cudaStream_t stream, const char** err) {
+                        int64_t Mp, int64_t Kp, const NhwcFeed& feed, cudaStream_t stream, const char** err) {
   constexpr int kBK = BF16 ? 64 : 32;
   auto enc = get_encode_fn();
   if (!enc) {
@@ -312,7 +317,11 @@ static int launch_shift(ShiftArgs a, const void* x_cl, const void* packed, int64
   const uint64_t tiles = static_cast<uint64_t>(a.n_tiles) * a.oh_tiles * a.ow_tiles * a.co_tiles;
   const uint32_t grid = tiles < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(tiles) : static_cast<uint32_t>(sms);
   im2win_note_kernel(RB ? "conv_tc_shift_kernel (window shift, filter resident)" : "conv_tc_shift_kernel (window shift)");
-  kern<<<grid, kTcThreads, smem, stream>>>(a, map_a, map_b);
+  e = launch_tc_kernel(kern, grid, smem, stream, feed.src != nullptr, a, map_a, map_b, feed);
+  if (e != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 2;
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
@@ -329,7 +338,8 @@ static int launch_shift(ShiftArgs a, const void* x_cl, const void* packed, int64
 // generic fused kernel, <0 on error.
 int im2win_try_conv_tc_shift(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n, int64_t c_in,
                              int64_t c_pad, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride, int bf16,
-                             double fused_util, cudaStream_t stream, const char** err) {
+                             double fused_util, const im2win::tc::NhwcFeed& feed, cudaStream_t stream,
+                             const char** err) {
   using namespace im2win::tc;
   if (stride != 1 || (w_f != 3 && w_f != 5)) return 0;
   const char* env = getenv("IM2WIN_SHIFT");
@@ -378,7 +388,7 @@ int im2win_try_conv_tc_shift(const void* x_cl, const float* flt, float* out, voi
   const bool rb = Mp == N && rb_bytes + 4 * kARows * kRowBytes + 1024 <= 227 * 1024 &&
                   !(getenv("IM2WIN_SHIFT_RB") && atoi(getenv("IM2WIN_SHIFT_RB")) == 0);
 #define IM2WIN_SH(BF, NN, ST, WFF, RBB) \
-  rc = launch_shift<BF, NN, ST, WFF, RBB>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, stream, err)
+  rc = launch_shift<BF, NN, ST, WFF, RBB>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err)
   if (w_f == 3) {
     if (bf16) {
       if (N == 64) { if (rb) IM2WIN_SH(true, 64, 4, 3, true); else IM2WIN_SH(true, 64, 5, 3, false); }

@@ -85,7 +85,9 @@ Geometry geometry(int64_t n_chunk, int64_t c_in, int64_t h, int64_t w, int64_t c
     g.conv_ws = im2win_conv_direct_workspace(c_in, c_out, h_f, w_f, variant);
   } else if (g.tc) {
     g.mid_bytes = static_cast<size_t>(n_chunk * (h + 2 * pad) * (w + 2 * pad) * g.pitch) * (variant == IM2WIN_BF16 ? 2 : 4);
-    g.conv_ws = im2win_conv_fused_workspace_bytes(c_in, c_out, h_f, w_f);
+    // unpadded: the one-call fused entry (channels-last copy inside the conv kernel or just before it)
+    g.conv_ws = pad == 0 ? im2win_conv_fused_nchw_workspace_bytes(n_chunk, c_in, c_out, h_f, w_f)
+                         : im2win_conv_fused_workspace_bytes(c_in, c_out, h_f, w_f);
   } else {
     g.mid_bytes = static_cast<size_t>(n_chunk * c_in * g.h_out * h_f * g.w_eff) * 4;
     g.conv_ws = im2win_conv_workspace_bytes(c_in, c_out, h_f, w_f, variant);
@@ -231,6 +233,11 @@ static int host_conv(const float* host_in, const float* host_flt, float* host_ou
       // the direct kernel reads the chunk's NCHW input itself: buffer s is free once it finishes
       rc = im2win_conv_direct(d_in[s], d_flt, d_out[s], nk, c_in, h, w, c_out, h_f, w_f, stride, pad, variant,
                               conv_ws, g.conv_ws, P.comp);
+      cudaEventRecord(P.xf_done[s], P.comp);
+    } else if (g.tc && pad == 0) {
+      // reads the chunk's NCHW input until the conv finishes: buffer s is free after it
+      rc = im2win_conv_fused_nchw(d_in[s], mid, d_flt, d_out[s], nk, c_in, h, w, c_out, h_f, w_f, stride, variant,
+                                  conv_ws, g.conv_ws, P.comp);
       cudaEventRecord(P.xf_done[s], P.comp);
     } else if (g.tc) {
       rc = im2win_nchw_to_nhwc_padded(d_in[s], mid, nk, c_in, h, w, variant == IM2WIN_BF16 ? 1 : 0, pad, P.comp);

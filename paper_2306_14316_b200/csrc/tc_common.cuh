@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "common.cuh"
 
 namespace im2win {
@@ -118,6 +120,193 @@ IM2WIN_DEVICE void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
           smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
       : "memory");
+}
+
+// ---------------------------------------------------------------- in-kernel channels-last feed
+// The TMA-fed kernels read a channels-last copy Xcl of the NCHW input.  Written by a separate
+// kernel, that copy costs a full HBM pass (0.42 of conv4's 1.17 ms in BF16) in series with
+// the conv.  With a feed, kFeedWarps extra warps per CTA of the conv kernel itself produce Xcl
+// while the tensor cores work: blocks of units of (image, channel group, pixel chunk) are dealt
+// to the feed warps of all CTAs round-robin, so the copy advances image by image in the order
+// the conv consumes it; each finished block bumps its image's ready counter with release
+// semantics.  The TMA producer waits
+// (acquire) for every image its next tile reads before issuing the loads.  CTAs wait on each
+// other, so the kernel is launched cooperatively (all CTAs co-resident, or no launch).
+// The ready counters are zeroed by the host before the launch (cudaMemsetAsync).
+constexpr int kFeedWarps = 8;
+constexpr int kTcThreadsFeed = kTcThreads + 32 * kFeedWarps;
+
+// A unit: G channels (one 32-byte run of Xcl per pixel) x 32*J pixels; each lane loads
+// G*J values (one coalesced 128-byte row per channel and j) before storing any.
+template <bool BF16>
+struct FeedShape {
+  static constexpr uint32_t G = BF16 ? 16 : 8;
+  static constexpr uint32_t J = BF16 ? 2 : 4;
+  static constexpr uint32_t kPix = 32 * J;
+};
+
+struct NhwcFeed {
+  const float* src;        // NCHW float32 input; nullptr: Xcl already exists, no feed
+  void* dst;               // Xcl [n][h*w][c_pad] (bf16 or f32)
+  uint32_t c_in, c_pad, hw, n_img;
+  uint32_t chunks;         // ceil(hw / kPix)
+  uint32_t units_per_img;  // chunks * ceil(c_pad / G)
+  uint32_t* ready;         // [n_img] finished units per image
+  uint32_t* next;          // unit claim counter
+  uint32_t nowait;         // A/B probe only (IM2WIN_FEED_NOWAIT): the producer does not wait
+};
+
+IM2WIN_DEVICE void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
+
+// One converter warp: blocks of kFeedBatch consecutive units (one image, mostly), dealt
+// round-robin.  Two units are in flight: the loads of unit i+1 are issued before unit i is
+// converted and stored.  The ready counter is bumped (after a fence) at the end of a block or
+// where a block crosses into the next image -- one fence round trip per block, not per unit.
+constexpr uint32_t kFeedBatch = 8;
+
+template <bool BF16>
+IM2WIN_DEVICE void feed_load(const NhwcFeed& f, uint32_t u, int lane, float (&v)[FeedShape<BF16>::J][FeedShape<BF16>::G]) {
+  using S = FeedShape<BF16>;
+  const uint32_t img = u / f.units_per_img;
+  const uint32_t r = u - img * f.units_per_img;
+  const uint32_t cg = (r / f.chunks) * S::G;
+  const uint32_t p0 = (r % f.chunks) * S::kPix;
+  const float* s = f.src + static_cast<uint64_t>(img) * f.c_in * f.hw;
+#pragma unroll
+  for (uint32_t c = 0; c < S::G; ++c)
+#pragma unroll
+    for (uint32_t j = 0; j < S::J; ++j) {
+      const uint32_t p = p0 + j * 32 + lane, ch = cg + c;
+      v[j][c] = (ch < f.c_in && p < f.hw) ? __ldcs(s + static_cast<uint64_t>(ch) * f.hw + p) : 0.0f;
+    }
+}
+
+template <bool BF16>
+IM2WIN_DEVICE void feed_store(const NhwcFeed& f, uint32_t u, int lane,
+                              const float (&v)[FeedShape<BF16>::J][FeedShape<BF16>::G]) {
+  using S = FeedShape<BF16>;
+  constexpr uint32_t kGran = BF16 ? 8 : 4;  // channels per 16-byte store
+  const uint32_t img = u / f.units_per_img;
+  const uint32_t r = u - img * f.units_per_img;
+  const uint32_t cg = (r / f.chunks) * S::G;
+  const uint32_t p0 = (r % f.chunks) * S::kPix;
+  const uint32_t grans = min(S::G, f.c_pad - cg) / kGran;
+#pragma unroll
+  for (uint32_t j = 0; j < S::J; ++j) {
+    const uint32_t p = p0 + j * 32 + lane;
+    if (p >= f.hw) continue;
+    const uint64_t o = (static_cast<uint64_t>(img) * f.hw + p) * f.c_pad + cg;
+#pragma unroll
+    for (uint32_t g = 0; g < S::G / kGran; ++g) {
+      if (g >= grans) break;
+      if constexpr (BF16) {
+        uint4 q;
+        q.x = pack_bf16x2(v[j][8 * g], v[j][8 * g + 1]);
+        q.y = pack_bf16x2(v[j][8 * g + 2], v[j][8 * g + 3]);
+        q.z = pack_bf16x2(v[j][8 * g + 4], v[j][8 * g + 5]);
+        q.w = pack_bf16x2(v[j][8 * g + 6], v[j][8 * g + 7]);
+        *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(f.dst) + o + 8 * g) = q;
+      } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(f.dst) + o + 4 * g) =
+            make_float4(v[j][4 * g], v[j][4 * g + 1], v[j][4 * g + 2], v[j][4 * g + 3]);
+      }
+    }
+  }
+}
+
+// Publish `count` finished units of image `img`: the TMA engine (async proxy) of another SM
+// reads these bytes next.
+IM2WIN_DEVICE void feed_publish(const NhwcFeed& f, uint32_t img, uint32_t count, int lane) {
+  fence_proxy_async_global();
+  __syncwarp();
+  if (lane == 0)
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(f.ready + img), "r"(count) : "memory");
+  __syncwarp();
+}
+
+template <bool BF16>
+IM2WIN_DEVICE void nhwc_feed_run(const NhwcFeed& f, int lane, uint32_t feed_warp, uint32_t feed_warps) {
+  using S = FeedShape<BF16>;
+  const uint32_t total = f.n_img * f.units_per_img;
+  // this warp's units: blocks of kFeedBatch consecutive units, every feed_warps-th block
+  auto step = [&](uint32_t u) { return (u + 1) % kFeedBatch ? u + 1 : u + 1 + (feed_warps - 1) * kFeedBatch; };
+  float va[S::J][S::G], vb[S::J][S::G];
+  uint32_t pend_img = 0, pend = 0;
+  uint32_t ua = feed_warp * kFeedBatch;
+  if (ua < total) feed_load<BF16>(f, ua, lane, va);
+  while (ua < total) {
+    const uint32_t ub = step(ua);
+    if (ub < total) feed_load<BF16>(f, ub, lane, vb);
+    const uint32_t img = ua / f.units_per_img;
+    if (pend && img != pend_img) {
+      feed_publish(f, pend_img, pend, lane);
+      pend = 0;
+    }
+    feed_store<BF16>(f, ua, lane, va);
+    pend_img = img;
+    ++pend;
+    if (ub != ua + 1 && pend) {  // end of a block
+      feed_publish(f, pend_img, pend, lane);
+      pend = 0;
+    }
+    if (ub >= total) break;
+    const uint32_t imgb = ub / f.units_per_img;
+    const uint32_t uc = step(ub);
+    if (uc < total) feed_load<BF16>(f, uc, lane, va);
+    if (pend && imgb != pend_img) {
+      feed_publish(f, pend_img, pend, lane);
+      pend = 0;
+    }
+    feed_store<BF16>(f, ub, lane, vb);
+    pend_img = imgb;
+    ++pend;
+    if (uc != ub + 1 && pend) {
+      feed_publish(f, pend_img, pend, lane);
+      pend = 0;
+    }
+    ua = uc;
+  }
+  if (pend) feed_publish(f, pend_img, pend, lane);
+}
+
+// Producer side: block until images [lo, hi] are complete.  [conf_lo, conf_hi] caches the
+// last confirmed contiguous range (tiles arrive in increasing image order per CTA).
+IM2WIN_DEVICE void nhwc_feed_wait(const NhwcFeed& f, uint32_t lo, uint32_t hi, uint32_t& conf_lo,
+                                  uint32_t& conf_hi) {
+  if (f.src == nullptr || f.nowait) return;
+  if (hi >= f.n_img) hi = f.n_img - 1;
+  bool waited = false;
+  for (uint32_t i = lo; i <= hi; ++i) {
+    if (i >= conf_lo && i <= conf_hi) continue;
+    uint32_t v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f.ready + i) : "memory");
+      if (v >= f.units_per_img) break;
+      __nanosleep(64);
+    }
+    waited = true;
+    if (conf_hi + 1 == i && conf_lo <= conf_hi) conf_hi = i;
+    else { conf_lo = i; conf_hi = i; }
+  }
+  if (waited) fence_proxy_async_global();
+}
+
+// Launch of a TMA-fed conv kernel: with a feed, the extra converter warps and a cooperative
+// launch (the CTAs wait on each other's feed units, so all must be co-resident).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_tc_kernel(void (*kern)(KArgs...), uint32_t grid, size_t smem, cudaStream_t stream,
+                                    bool feed, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(feed ? kTcThreadsFeed : kTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = feed ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 inline PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {

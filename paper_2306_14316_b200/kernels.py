@@ -207,6 +207,32 @@ def conv_fused_into(x_nhwc: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, 
     _lib.check(rc)
 
 
+def conv_fused_nchw_into(x: torch.Tensor, x_nhwc: torch.Tensor, flt: torch.Tensor, out: torch.Tensor,
+                         params: ConvParams, variant: str, ws: torch.Tensor | None = None) -> None:
+    """The fused tensor-core conv straight from the NCHW input: extra warps of the conv kernel
+    write the channels-last scratch ``x_nhwc`` while the tensor cores consume it (no separate
+    copy kernel).  Same bits as ``nhwc_into`` + ``conv_fused_into``."""
+    n_img, c_in, h_in, w_in = (int(d) for d in x.shape)
+    code = _variant_code(variant)
+    lib = _lib.load()
+    nbytes = lib.im2win_conv_fused_nchw_workspace_bytes(n_img, c_in, params.c_out, params.h_f, params.w_f)
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    ws = _workspace(out.device, stream, nbytes) if ws is None else _check_ws(ws, nbytes)
+    with torch.cuda.device(out.device):
+        rc = lib.im2win_conv_fused_nchw(x.data_ptr(), x_nhwc.data_ptr(), flt.data_ptr(), out.data_ptr(), n_img,
+                                        c_in, h_in, w_in, params.c_out, params.h_f, params.w_f, params.stride, code,
+                                        ws.data_ptr(), ws.numel(), stream)
+    _lib.check(rc)
+
+
+def feed_enabled(params: ConvParams) -> bool:
+    """Whether the fused path goes through the one-call entry (im2win_conv_fused_nchw), where the
+    library either produces the channels-last copy inside the conv kernel or runs its copy
+    kernel first (rule and IM2WIN_FEED switch in conv_tc_fused.cu).  Zero padding keeps the
+    two-call form, whose copy kernel writes the border."""
+    return params.pad == 0
+
+
 def direct_supported(inp_dims, params: ConvParams, variant: str) -> bool:
     """Whether the in-SM im2win tensor-core kernel (few-channel inputs) covers this shape."""
     if variant not in ("tf32", "bf16"):
@@ -280,10 +306,13 @@ def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, 
         pad = params.pad
         x_cl = torch.empty((n_img, h_in + 2 * pad, w_in + 2 * pad, nhwc_pitch(c_in, variant)), dtype=dt,
                            device=i.device)
-        nhwc_into(i.data, x_cl, pad)
         out = torch.empty((n_img, params.c_out, h_out, w_out), dtype=DTYPE, device=i.device)
         fd = f.data if f.device == i.device else f.data.to(i.device)
-        conv_fused_into(x_cl, fd, out, params, variant)
+        if feed_enabled(params):
+            conv_fused_nchw_into(i.data, x_cl, fd, out, params, variant)
+        else:
+            nhwc_into(i.data, x_cl, pad)
+            conv_fused_into(x_cl, fd, out, params, variant)
         return Tensor4(out)
     if ok and tc_path == "cl" and params.pad:
         raise ValueError("tc_path='cl' has no zero padding; use 'fused' or 'gather'")
@@ -490,7 +519,7 @@ class CapturedConv:
         lib = _lib.load()
         code = _variant_code(variant)
         ws_bytes = max(lib.im2win_conv_workspace_bytes(c_in, params.c_out, params.h_f, params.w_f, code),
-                       lib.im2win_conv_fused_workspace_bytes(c_in, params.c_out, params.h_f, params.w_f),
+                       lib.im2win_conv_fused_nchw_workspace_bytes(n_img, c_in, params.c_out, params.h_f, params.w_f),
                        lib.im2win_conv_direct_workspace(c_in, params.c_out, params.h_f, params.w_f, code))
         self._ws = torch.empty(max(ws_bytes, 1 << 16), dtype=torch.uint8, device=dev)
         if variant in ("tf32", "bf16") and direct_preferred(self.input.shape, params, variant):
@@ -502,9 +531,13 @@ class CapturedConv:
             self._mid = torch.empty((n_img, h_in + 2 * pad, w_in + 2 * pad, nhwc_pitch(c_in, variant)), dtype=dt,
                                     device=dev)
 
-            def body():
-                nhwc_into(self.input, self._mid, pad)
-                conv_fused_into(self._mid, self.filter, self.out, params, variant, self._ws)
+            if feed_enabled(params):
+                def body():
+                    conv_fused_nchw_into(self.input, self._mid, self.filter, self.out, params, variant, self._ws)
+            else:
+                def body():
+                    nhwc_into(self.input, self._mid, pad)
+                    conv_fused_into(self._mid, self.filter, self.out, params, variant, self._ws)
         else:
             from .layouts import effective_width, im2win_into
 

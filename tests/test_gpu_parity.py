@@ -738,3 +738,67 @@ def test_reference_harness_call_and_search_plan(layer_goldens):
         pkg.TilePlan(64, 64, 16, 4, 4)]
     abl = pkg.run_ablation(replace(cfg, batch=4, repeats=1))
     assert len({r.checksum for r in abl}) == 1
+
+
+def _feed_vs_copy(inp, flt, params, variant, monkeypatch):
+    """conv_im2win_opt with the in-kernel feed forced vs with the copy kernel forced: same bits."""
+    monkeypatch.setenv("IM2WIN_FEED", "2")
+    fed = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path="fused").numpy()
+    monkeypatch.setenv("IM2WIN_FEED", "0")
+    copied = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path="fused").numpy()
+    monkeypatch.delenv("IM2WIN_FEED")
+    return fed, copied
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+@pytest.mark.parametrize("select", ["auto", "phase", "shift", "generic"])
+def test_tc_feed_bitwise_all_layers(select, variant, layer_goldens, monkeypatch):
+    """The channels-last copy produced by the conv kernel's own feed warps (im2win_conv_fused_nchw)
+    gives the same bits as the separate copy kernel, for every TMA-fed kernel and layer; and the
+    result is within the stated tolerance of the reference golden's oracle."""
+    env = {"auto": ("1", "1"), "phase": ("2", "0"), "shift": ("0", "2"), "generic": ("0", "0")}[select]
+    monkeypatch.setenv("IM2WIN_PHASE", env[0])
+    monkeypatch.setenv("IM2WIN_SHIFT", env[1])
+    for name in BENCHMARKS:
+        g = layer_goldens[name]
+        cfg = replace(BENCHMARKS[name], batch=g["batch"], seed=g["seed"])
+        inp, flt = make_inputs(cfg)
+        fed, copied = _feed_vs_copy(inp, flt, cfg.params, variant, monkeypatch)
+        assert bits_equal(fed, copied), (name, select)
+        assert pkg.normalized_max_diff(fed, orc.conv_direct(inp, flt, cfg.stride)) <= TC_TOL[variant], (name, select)
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_tc_feed_ragged_geometries(variant, monkeypatch):
+    """Feed units on ragged shapes: pixel counts not a multiple of the unit's 64/128 pixels, channel
+    counts not a multiple of the 8/16-channel group (and below the 16-byte pitch), one image, many
+    images smaller than a unit, the phase kernel's multi-image tiles."""
+    cases = [(3, 64, 17, 19, 64, 7, 7, 2), (2, 40, 12, 13, 128, 3, 3, 1), (1, 3, 30, 33, 64, 3, 3, 1),
+             (9, 72, 7, 7, 96, 3, 3, 1), (4, 130, 9, 10, 256, 3, 3, 1), (1, 64, 140, 140, 64, 7, 7, 2),
+             (7, 16, 5, 6, 64, 3, 3, 1)]
+    for (n, c, h, w, co, hf, wf, s) in cases:
+        rng = np.random.default_rng(n * 1000 + h + c)
+        inp = rng.standard_normal((n, c, h, w), dtype=np.float32)
+        flt = rng.standard_normal((co, c, hf, wf), dtype=np.float32)
+        params = pkg.ConvParams(c, co, hf, wf, s)
+        fed, copied = _feed_vs_copy(inp, flt, params, variant, monkeypatch)
+        assert bits_equal(fed, copied), (n, c, h, w, co, hf, wf, s)
+        assert pkg.normalized_max_diff(fed, orc.conv_direct(inp, flt, s)) <= TC_TOL[variant], (n, c, h, w)
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_tc_feed_conv4_n128_sampled_images(variant):
+    """The auto rule feeds conv4 (output/input elements 0.24): at N=128 every sampled image
+    matches the oracle within tolerance (images are independent, reference.py:78-90)."""
+    cfg = replace(BENCHMARKS["conv4"], batch=128)
+    g = torch.Generator(device=DEV).manual_seed(44)
+    x = torch.randn((128, cfg.c_in, cfg.h_in, cfg.w_in), device=DEV, generator=g)
+    f = torch.randn((cfg.c_out, cfg.c_in, cfg.h_f, cfg.w_f), device=DEV, generator=g)
+    out = pkg.conv_im2win_opt(x, f, cfg.params, variant=variant)
+    from paper_2306_14316_b200 import _lib
+
+    assert "phase" in _lib.last_kernel()
+    fn = f.cpu().numpy()
+    for i in (0, 1, 63, 127):
+        ref = orc.conv_direct(x[i:i + 1].cpu().numpy(), fn, cfg.stride)
+        assert pkg.normalized_max_diff(out.data[i:i + 1].cpu().numpy(), ref) <= TC_TOL[variant], i
