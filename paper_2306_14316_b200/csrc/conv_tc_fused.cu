@@ -462,7 +462,7 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
                               : "conv_tc_fused_kernel (generic TMA window boxes, filter resident, tf32)")
                      : (BF16 ? "conv_tc_fused_kernel (generic TMA window boxes, bf16)"
                              : "conv_tc_fused_kernel (generic TMA window boxes, tf32)"));
-  e = launch_tc_kernel(kern, grid, smem, stream, feed.src != nullptr, a, map_a, map_b, feed);
+  e = launch_tc_kernel(kern, grid, smem, stream, feed.src != nullptr, 1, a, map_a, map_b, feed);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);

@@ -38,20 +38,26 @@ struct PhaseArgs {
 
 constexpr int kPhRows = 136;  // 128 MMA rows + up to 8 rows of shift
 
-template <bool BF16, int N, int STAGES, int TAPS, int MT>
+// PAIR: a 2-CTA cluster runs UMMA M = 256 (cta_group::2): each CTA stages its own MT pixel
+// tiles and half of each filter tap (N/2 rows), so the per-SM shared-memory operand bytes per
+// MMA drop from (128 + N) to (128 + N/2) rows and the filter's L2->SM traffic halves.  Work
+// items are then 2*MT pixel tiles (MT per CTA).  Rank 0 issues the MMAs.
+template <bool BF16, int N, int STAGES, int TAPS, int MT, bool PAIR>
 __global__ void __launch_bounds__(kTcThreadsFeed, 1)
     conv_tc_phase_kernel(const PhaseArgs a, const __grid_constant__ CUtensorMap tmap_a0,
                          const __grid_constant__ CUtensorMap tmap_a1, const __grid_constant__ CUtensorMap tmap_b,
                          const NhwcFeed feed) {
   constexpr uint32_t kATile = kPhRows * kRowBytes;  // 17 KB, multiple of 1024
   constexpr uint32_t kABytes = MT * kATile;
-  constexpr uint32_t kBTap = N * kRowBytes;
+  constexpr int kBRows = PAIR ? N / 2 : N;           // filter rows staged by this CTA
+  constexpr uint32_t kBTap = kBRows * kRowBytes;
   constexpr uint32_t kStageBytes = kABytes + TAPS * kBTap;
   constexpr int kBK = BF16 ? 64 : 32;
   constexpr int kUK = BF16 ? 16 : 8;
   constexpr uint32_t kTmemCols = (2 * MT * N <= 128) ? 128 : (2 * MT * N <= 256 ? 256 : 512);
-  constexpr uint32_t kIdesc = instr_desc<BF16, N>();
-  static_assert(kATile % 1024 == 0, "A tiles must keep 1024 B alignment");
+  constexpr uint32_t kIdesc = instr_desc_m<BF16, N, PAIR ? 256 : 128>();
+  constexpr uint32_t kCtas = PAIR ? 2 : 1;
+  static_assert(kATile % 1024 == 0 && kBTap % 1024 == 0, "tiles must keep 1024 B alignment");
   static_assert(2 * MT * N <= 512, "TMEM holds 512 fp32 columns");
 
   extern __shared__ uint8_t smem_raw[];
@@ -67,6 +73,8 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
   const uint32_t loaded_rows = a.pitch * a.rows * a.box_n;
   const uint32_t a_box_bytes = loaded_rows * kRowBytes;
   const uint32_t s = a.stride;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const uint32_t unit = blockIdx.x / kCtas, units = gridDim.x / kCtas;  // CTA or CTA pair
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -75,7 +83,7 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], kEpiWarps);
+      mbar_init(&tempty_bar[i], kCtas * kEpiWarps);
     }
     fence_barrier_init();
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap_a0) : "memory");
@@ -83,9 +91,17 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap_b) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                       smem_u32(&tmem_base_sh)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                       smem_u32(&tmem_base_sh)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
   }
   // rows past the TMA box feed only padding D rows; keep them finite
   for (uint32_t i = threadIdx.x; i < STAGES * kStageBytes / 16; i += blockDim.x)
@@ -93,6 +109,7 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // the peer's barriers are initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_sh;
   const uint32_t total = a.pairs * a.co_tiles;
@@ -101,14 +118,14 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       uint32_t conf_lo = 1, conf_hi = 0;
-      for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+      for (uint32_t t = unit; t < total; t += units) {
         const uint32_t co_blk = t % a.co_tiles;
         const uint32_t pair = t / a.co_tiles;
         uint32_t ow0[MT], oh0[MT], n0[MT];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           // past the last pixel tile: coordinates past the tensor (TMA zero-fills), D not stored
-          uint32_t pt = pair * MT + mt;
+          uint32_t pt = (pair * kCtas + rank) * MT + mt;
           ow0[mt] = (pt % a.ow_tiles) * a.box_w;
           pt /= a.ow_tiles;
           oh0[mt] = (pt % a.oh_tiles) * a.rows;
@@ -123,28 +140,49 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
           const uint32_t nq = (a.w_f - r + s - 1) / s;
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * kStageBytes;
-          mbar_arrive_expect_tx(&full_bar[stage], MT * a_box_bytes + nq * kBTap);
           const CUtensorMap* am = r == 0 ? &tmap_a0 : &tmap_a1;
+          if constexpr (PAIR) {
+            // both CTAs' loads complete on rank 0's full barrier, which expects the bytes of both
+            if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (MT * a_box_bytes + nq * kBTap));
+            const uint32_t fb = mapa_shared(&full_bar[stage], 0);
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            asm volatile(
-                "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
-                "%6, %7}], [%2];\n" ::"r"(smem_u32(st + mt * kATile)),
-                "l"(am), "r"(smem_u32(&full_bar[stage])), "r"(c0), "r"(ow0[mt]), "r"(fh % s), "r"(oh0[mt] + fh / s),
-                "r"(n0[mt])
-                : "memory");
+            for (int mt = 0; mt < MT; ++mt) {
+              asm volatile(
+                  "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+                  "[%1, {%3, %4, %5, %6, %7}], [%2];\n" ::"r"(smem_u32(st + mt * kATile)),
+                  "l"(am), "r"(fb), "r"(c0), "r"(ow0[mt]), "r"(fh % s), "r"(oh0[mt] + fh / s), "r"(n0[mt])
+                  : "memory");
+            }
+            for (uint32_t q = 0; q < nq; ++q)
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+                  "[%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(st + kABytes + q * kBTap)),
+                  "l"(&tmap_b), "r"(fb), "r"((fh * a.w_f + s * q + r) * a.c_slabs * kBK + c0),
+                  "r"(co_blk * N + rank * kBRows)
+                  : "memory");
+          } else {
+            mbar_arrive_expect_tx(&full_bar[stage], MT * a_box_bytes + nq * kBTap);
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              asm volatile(
+                  "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+                  "%5, %6, %7}], [%2];\n" ::"r"(smem_u32(st + mt * kATile)),
+                  "l"(am), "r"(smem_u32(&full_bar[stage])), "r"(c0), "r"(ow0[mt]), "r"(fh % s),
+                  "r"(oh0[mt] + fh / s), "r"(n0[mt])
+                  : "memory");
+            }
+            for (uint32_t q = 0; q < nq; ++q)
+              tma_load_2d(st + kABytes + q * kBTap, &tmap_b, &full_bar[stage],
+                          (fh * a.w_f + s * q + r) * a.c_slabs * kBK + c0, co_blk * N);
           }
-          for (uint32_t q = 0; q < nq; ++q)
-            tma_load_2d(st + kABytes + q * kBTap, &tmap_b, &full_bar[stage],
-                        (fh * a.w_f + s * q + r) * a.c_slabs * kBK + c0, co_blk * N);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+      for (uint32_t t = unit; t < total; t += units) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * (MT * N);
@@ -162,16 +200,24 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
               for (int kk = 0; kk < kBK / kUK; ++kk) {
                 const uint64_t bd = smem_desc_sw128(bbase + q * kBTap + kk * 32);
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt)
-                  mma<BF16>(tmem_d + mt * N, smem_desc_sw128(abase + mt * kATile + q * kRowBytes + kk * 32), bd,
-                            kIdesc, (ki | q | kk) != 0);
+                for (int mt = 0; mt < MT; ++mt) {
+#ifdef IM2WIN_PHASE_NOSHIFT  // exploration builds only: wrong results, times an unshifted A read
+                  const uint64_t ad = smem_desc_sw128(abase + mt * kATile + kk * 32);
+#else
+                  const uint64_t ad = smem_desc_sw128(abase + mt * kATile + q * kRowBytes + kk * 32);
+#endif
+                  if constexpr (PAIR) mma_pair<BF16>(tmem_d + mt * N, ad, bd, kIdesc, (ki | q | kk) != 0);
+                  else mma<BF16>(tmem_d + mt * N, ad, bd, kIdesc, (ki | q | kk) != 0);
+                }
               }
             }
           }
-          mma_commit(&empty_bar[stage]);
+          if constexpr (PAIR) mma_commit_pair(&empty_bar[stage]);
+          else mma_commit(&empty_bar[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull_bar[acc]);
+        if constexpr (PAIR) mma_commit_pair(&tfull_bar[acc]);
+        else mma_commit(&tfull_bar[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -187,14 +233,14 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
     const uint32_t r_n = rr / per_img, r_rem = rr % per_img;
     const uint32_t r_h = r_rem / a.pitch, r_w = r_rem % a.pitch;
     uint32_t acc = 0, acc_phase = 0;
-    for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+    for (uint32_t t = unit; t < total; t += units) {
       const uint32_t co_blk = t % a.co_tiles;
       const uint32_t pair = t / a.co_tiles;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
-        uint32_t pt = pair * MT + mt;
+        uint32_t pt = (pair * kCtas + rank) * MT + mt;
         const bool tile_ok = pt < a.p_tiles;
         const uint32_t ow = (pt % a.ow_tiles) * a.box_w + r_w;
         pt /= a.ow_tiles;
@@ -211,25 +257,36 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
           uint32_t v[16];
           tmem_ld16(taddr + j0, v);
           const uint32_t m0 = co_blk * N + j0;
+#ifndef IM2WIN_PHASE_NOSTORE  // exploration builds only: times the kernel without its output stores
           if (valid) {
 #pragma unroll
             for (int q = 0; q < 16; ++q)
               if (m0 + q < a.co) a.out[obase + static_cast<int64_t>(m0 + q) * a.hw] = __uint_as_float(v[q]);
           }
+#else
+          if (valid && v[0] == 0x7fffffffu) a.out[obase] = 0.f;
+#endif
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if (PAIR && rank != 0) mbar_arrive_remote(mapa_shared(&tempty_bar[acc], 0));
+        else mbar_arrive(&tempty_bar[acc]);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // no CTA frees TMEM or exits while its peer may still signal it
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(kTmemCols));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(kTmemCols));
   }
 }
 
@@ -254,7 +311,7 @@ inline double phase_tile(int64_t n, int64_t h_out, int64_t w_out, int64_t qmax, 
   return static_cast<double>(a.box_w) * a.rows * a.box_n / kTileM;
 }
 
-template <bool BF16, int N, int STAGES, int TAPS, int MT>
+template <bool BF16, int N, int STAGES, int TAPS, int MT, bool PAIR = false>
 static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64_t c_pad, int64_t h, int64_t w,
                         int64_t Mp, int64_t Kp, const NhwcFeed& feed, cudaStream_t stream, const char** err) {
   constexpr int kBK = BF16 ? 64 : 32;
@@ -287,7 +344,7 @@ static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64
   {
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(Mp)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(Kp) * esz};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(N)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(PAIR ? N / 2 : N)};
     cuuint32_t estr[2] = {1, 1};
     CUresult res = enc(&map_b, dt, 2, const_cast<void*>(packed), dims, strides, box, estr,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -298,8 +355,8 @@ static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64
     }
   }
   a.co_tiles = static_cast<uint32_t>(Mp / N);
-  const size_t smem = static_cast<size_t>(STAGES) * (MT * kPhRows + TAPS * N) * kRowBytes + 1024;
-  auto kern = conv_tc_phase_kernel<BF16, N, STAGES, TAPS, MT>;
+  const size_t smem = static_cast<size_t>(STAGES) * (MT * kPhRows + TAPS * (PAIR ? N / 2 : N)) * kRowBytes + 1024;
+  auto kern = conv_tc_phase_kernel<BF16, N, STAGES, TAPS, MT, PAIR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
@@ -309,9 +366,22 @@ static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t items = static_cast<uint64_t>(a.pairs) * a.co_tiles;
-  const uint32_t grid = items < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(items) : static_cast<uint32_t>(sms);
-  im2win_note_kernel(MT == 4 ? "conv_tc_phase_kernel (phase shift, 4 tiles/item)" : "conv_tc_phase_kernel (phase shift, 2 tiles/item)");
-  e = launch_tc_kernel(kern, grid, smem, stream, feed.src != nullptr, a, map_a[0], map_a[1], map_b, feed);
+  uint32_t grid = items < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(items) : static_cast<uint32_t>(sms);
+  if constexpr (PAIR) {
+    const int clusters = max_pair_clusters(kern, smem, feed.src != nullptr);
+    if (clusters < 1) {
+      *err = "conv_tc_phase: no 2-CTA cluster fits";
+      return 2;
+    }
+    grid = 2 * static_cast<uint32_t>(std::min<uint64_t>(items, static_cast<uint64_t>(clusters)));
+    im2win_note_kernel(MT == 4 ? "conv_tc_phase_kernel (phase shift, CTA pair M=256, 4 tiles/CTA)"
+                               : "conv_tc_phase_kernel (phase shift, CTA pair M=256, 2 tiles/CTA)");
+  } else {
+    im2win_note_kernel(MT == 4 ? "conv_tc_phase_kernel (phase shift, 4 tiles/item)"
+                               : "conv_tc_phase_kernel (phase shift, 2 tiles/item)");
+  }
+  e = launch_tc_kernel(kern, grid, smem, stream, feed.src != nullptr, PAIR ? 2 : 1, a, map_a[0], map_a[1], map_b,
+                       feed);
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
     return 2;
@@ -400,7 +470,14 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
   const char* mt_env = getenv("IM2WIN_PHASE_MT");
   int mt_sel = (N == 64 && taps <= 5) ? 4 : 2;
   if (mt_env && (atoi(mt_env) == 2 || (atoi(mt_env) == 4 && N == 64 && taps <= 5))) mt_sel = atoi(mt_env);
-  a.pairs = (a.p_tiles + mt_sel - 1) / mt_sel;
+  // CTA pairs (cta_group::2, M = 256): IM2WIN_PAIR=1 turns them on; off by default.  Measured
+  // (tools/probes/umma_rate.cu, B200): a 128x64x16 BF16 UMMA from shared memory takes 48 cycles
+  // (operand-read bound: 6 KB at 128 B/clk; 32 cycles of math), the pair's 256x64x16 44.6 --
+  // the B half the pair saves is not what bounds it, and conv4/conv9 time the same with and
+  // without pairs (BF16 conv4 0.819 vs 0.811 ms, N=128); conv8 TF32 (N=128) 2% faster.
+  const char* pair_env = getenv("IM2WIN_PAIR");
+  const bool pair = pair_env && atoi(pair_env) > 0;
+  a.pairs = (a.p_tiles + mt_sel * (pair ? 2 : 1) - 1) / (mt_sel * (pair ? 2 : 1));
   a.stride = static_cast<uint32_t>(stride);
   a.w_f = static_cast<uint32_t>(w_f);
   a.c_slabs = static_cast<uint32_t>(c_slabs);
@@ -415,8 +492,9 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
                                                              static_cast<int>(Kc));
   int rc = 1;
   // stage = 2 x 17 KB of A + taps x N x 128 B of B; as many stages as fit in 227 KB
-#define IM2WIN_PH(BF, NN, ST, TP) \
-  rc = launch_phase<BF, NN, ST, TP, 2>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err)
+#define IM2WIN_PH(BF, NN, ST, TP)                                                                             \
+  rc = pair ? launch_phase<BF, NN, ST, TP, 2, true>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err) \
+            : launch_phase<BF, NN, ST, TP, 2>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err)
 #define IM2WIN_PH_T(BF)                                        \
   switch (taps * 1000 + N) {                                   \
     case 2064: IM2WIN_PH(BF, 64, 4, 2); break;                 \
@@ -431,12 +509,15 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
   }
   if (mt_sel == 4) {
     // stage = 4 x 17 KB of A + taps x 8 KB of B: two stages
-#define IM2WIN_PH4(BF)                                                                                   \
-  switch (taps) {                                                                                        \
-    case 2: rc = launch_phase<BF, 64, 2, 2, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err); break; \
-    case 3: rc = launch_phase<BF, 64, 2, 3, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err); break; \
-    case 4: rc = launch_phase<BF, 64, 2, 4, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err); break; \
-    default: rc = launch_phase<BF, 64, 2, 5, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err); break; \
+#define IM2WIN_PH4_T(BF, TP)                                                                                \
+  rc = pair ? launch_phase<BF, 64, 2, TP, 4, true>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err) \
+            : launch_phase<BF, 64, 2, TP, 4>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err)
+#define IM2WIN_PH4(BF)                          \
+  switch (taps) {                               \
+    case 2: IM2WIN_PH4_T(BF, 2); break;         \
+    case 3: IM2WIN_PH4_T(BF, 3); break;         \
+    case 4: IM2WIN_PH4_T(BF, 4); break;         \
+    default: IM2WIN_PH4_T(BF, 5); break;        \
   }
     if (bf16) {
       IM2WIN_PH4(true)
@@ -444,6 +525,7 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
       IM2WIN_PH4(false)
     }
 #undef IM2WIN_PH4
+#undef IM2WIN_PH4_T
   } else if (bf16) {
     IM2WIN_PH_T(true)
   } else {

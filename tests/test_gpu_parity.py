@@ -802,3 +802,36 @@ def test_tc_feed_conv4_n128_sampled_images(variant):
     for i in (0, 1, 63, 127):
         ref = orc.conv_direct(x[i:i + 1].cpu().numpy(), fn, cfg.stride)
         assert pkg.normalized_max_diff(out.data[i:i + 1].cpu().numpy(), ref) <= TC_TOL[variant], i
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_tc_phase_cta_pair(variant, layer_goldens, monkeypatch):
+    """The phase kernel on CTA pairs (cta_group::2, UMMA M = 256, filter halves per CTA,
+    IM2WIN_PAIR=1) is within tolerance on every layer it takes and on ragged geometries (odd
+    pixel-tile counts leave the second CTA's tiles empty), with and without the feed."""
+    monkeypatch.setenv("IM2WIN_PAIR", "1")
+    monkeypatch.setenv("IM2WIN_PHASE", "2")
+    monkeypatch.setenv("IM2WIN_SHIFT", "0")
+    from paper_2306_14316_b200 import _lib
+
+    for name in BENCHMARKS:
+        g = layer_goldens[name]
+        cfg = replace(BENCHMARKS[name], batch=g["batch"], seed=g["seed"])
+        inp, flt = make_inputs(cfg)
+        ref = orc.conv_direct(inp, flt, cfg.stride)
+        for feed in ("0", "2"):
+            monkeypatch.setenv("IM2WIN_FEED", feed)
+            out = pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant, tc_path="fused").numpy()
+            assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (name, feed)
+    cases = [(3, 64, 17, 19, 64, 7, 7, 2), (1, 64, 23, 9, 64, 3, 3, 2), (2, 40, 12, 13, 128, 3, 3, 1),
+             (5, 32, 8, 8, 64, 5, 5, 1)]
+    seen = set()
+    for (n, c, h, w, co, hf, wf, s) in cases:
+        rng = np.random.default_rng(n * 1000 + h)
+        inp = rng.standard_normal((n, c, h, w), dtype=np.float32)
+        flt = rng.standard_normal((co, c, hf, wf), dtype=np.float32)
+        out = pkg.conv_im2win_opt(inp, flt, pkg.ConvParams(c, co, hf, wf, s), variant=variant,
+                                  tc_path="fused").numpy()
+        seen.add(_lib.last_kernel())
+        assert pkg.normalized_max_diff(out, orc.conv_direct(inp, flt, s)) <= TC_TOL[variant], (n, c, h, w)
+    assert any("CTA pair" in k for k in seen), seen
