@@ -238,6 +238,10 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
       const uint32_t pair = t / a.co_tiles;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      // the MT tiles' pieces of each channel plane are stored back to back (consecutive output
+      // rows of a plane: longer DRAM write runs, tools/probes/nchw_store_probe.cu)
+      int64_t obase[MT];
+      bool valid[MT];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         uint32_t pt = (pair * kCtas + rank) * MT + mt;
@@ -246,27 +250,29 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
         pt /= a.ow_tiles;
         const uint32_t oh = (pt % a.oh_tiles) * a.rows + r_h;
         const uint32_t img = (pt / a.oh_tiles) * a.box_n + r_n;
-        const bool valid =
-            tile_ok && rr < loaded_rows && r_w < a.box_w && ow < a.w_out && oh < a.h_out && img < a.n_img;
-        const int64_t obase =
-            valid ? static_cast<int64_t>(img) * a.co * a.hw + static_cast<int64_t>(oh) * a.w_out + ow : 0;
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * (MT * N) + mt * N;
+        valid[mt] = tile_ok && rr < loaded_rows && r_w < a.box_w && ow < a.w_out && oh < a.h_out && img < a.n_img;
+        obase[mt] = valid[mt] ? static_cast<int64_t>(img) * a.co * a.hw + static_cast<int64_t>(oh) * a.w_out + ow : 0;
+      }
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * (MT * N);
 #pragma unroll
-        for (int jj = 0; jj < N / 2; jj += 16) {
-          const int j0 = j_lo + jj;
-          uint32_t v[16];
-          tmem_ld16(taddr + j0, v);
-          const uint32_t m0 = co_blk * N + j0;
+      for (int jj = 0; jj < N / 2; jj += 16) {
+        const int j0 = j_lo + jj;
+        uint32_t v[MT][16];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) tmem_ld16(taddr + mt * N + j0, v[mt]);
+        const uint32_t m0 = co_blk * N + j0;
 #ifndef IM2WIN_PHASE_NOSTORE  // exploration builds only: times the kernel without its output stores
-          if (valid) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-              if (m0 + q < a.co) a.out[obase + static_cast<int64_t>(m0 + q) * a.hw] = __uint_as_float(v[q]);
+        for (int q = 0; q < 16; ++q) {
+          if (m0 + q < a.co) {
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+              if (valid[mt]) a.out[obase[mt] + static_cast<int64_t>(m0 + q) * a.hw] = __uint_as_float(v[mt][q]);
           }
-#else
-          if (valid && v[0] == 0x7fffffffu) a.out[obase] = 0.f;
-#endif
         }
+#else
+        if (valid[0] && v[0][0] == 0x7fffffffu) a.out[obase[0]] = 0.f;
+#endif
       }
       tc_fence_before();
       __syncwarp();
