@@ -392,6 +392,15 @@ def roofline_row(flops: float, nbytes: float, seconds: float, peak_tf: float, hb
             "frac": achieved / attainable, "alg_bytes": nbytes}
 
 
+def _feed_chosen(cfg, variant: str) -> bool:
+    """Mirror of the library's feed rule (conv_tc_fused.cu): the channels-last copy is produced
+    inside the conv kernel when output/input elements <= 0.5 and N <= 512, or when IM2WIN_FEED=2."""
+    mode = os.environ.get("IM2WIN_FEED", "1")
+    h_out, w_out = cfg.out_dims
+    r = cfg.c_out * h_out * w_out / (cfg.c_in * cfg.h_in * cfg.w_in)
+    return mode == "2" or (mode == "1" and r <= 0.5 and cfg.batch <= 512)
+
+
 def tc_layer(D, cfg_global, variant: str, reps: int = 5) -> dict:
     """Time the production TF32/BF16 path for one layer at a global batch split over the ranks.
 
@@ -405,8 +414,8 @@ def tc_layer(D, cfg_global, variant: str, reps: int = 5) -> dict:
     from paper_2306_14316_b200.kernels import (
         conv_direct_into,
         conv_fused_into,
+        conv_fused_nchw_into,
         direct_preferred,
-        nhwc_into,
         nhwc_pitch,
     )
     from paper_2306_14316_b200.sharding import shard_bounds
@@ -428,20 +437,25 @@ def tc_layer(D, cfg_global, variant: str, reps: int = 5) -> dict:
     if direct_preferred(x.shape, cfg.params, variant):
         ws = torch.empty(max(lib.im2win_conv_direct_workspace(cfg.c_in, cfg.c_out, cfg.h_f, cfg.w_f, code), 1 << 16),
                          dtype=torch.uint8, device=dev)
-        tr = None
+        one = None
         cv = lambda: conv_direct_into(x, f, o, cfg.params, variant, ws)  # noqa: E731
         cv()
         path = _lib.last_kernel()
     else:
-        ws = torch.empty(max(lib.im2win_conv_fused_workspace_bytes(cfg.c_in, cfg.c_out, cfg.h_f, cfg.w_f), 1 << 16),
+        # production: one call (im2win_conv_fused_nchw) -- the library produces the channels-last
+        # copy inside the conv kernel (feed) or with its copy kernel just before it; "conv" times
+        # the conv kernel alone on an existing copy
+        ws = torch.empty(max(lib.im2win_conv_fused_nchw_workspace_bytes(cfg.batch, cfg.c_in, cfg.c_out, cfg.h_f,
+                                                                        cfg.w_f), 1 << 16),
                          dtype=torch.uint8, device=dev)
         w = torch.empty((cfg.batch, cfg.h_in, cfg.w_in, nhwc_pitch(cfg.c_in, variant)),
                         dtype=torch.bfloat16 if variant == "bf16" else torch.float32, device=dev)
-        tr = lambda: nhwc_into(x, w)  # noqa: E731
+        one = lambda: conv_fused_nchw_into(x, w, f, o, cfg.params, variant, ws)  # noqa: E731
         cv = lambda: conv_fused_into(w, f, o, cfg.params, variant, ws)  # noqa: E731
-        tr()
+        one()
+        path = "one call (" + ("in-kernel NHWC feed" if _feed_chosen(cfg, variant) else "NHWC copy kernel") + ") + " \
+            + _lib.last_kernel()
         cv()
-        path = "nhwc copy + " + _lib.last_kernel()
     torch.cuda.synchronize(dev)
     peak_mem = torch.cuda.max_memory_allocated(dev) - base
 
@@ -458,7 +472,7 @@ def tc_layer(D, cfg_global, variant: str, reps: int = 5) -> dict:
                 fn()
         return gr
 
-    g_all = capture([fn for fn in (tr, cv) if fn is not None])
+    g_all = capture([one] if one is not None else [cv])
     g_cv = capture([cv])
     times = {}
     for key, gr in (("all", g_all), ("conv", g_cv)):
@@ -506,6 +520,7 @@ def main() -> None:
     from paper_2306_14316_b200.kernels import (
         conv_direct_into,
         conv_fused_into,
+        conv_fused_nchw_into,
         conv_windows_into,
         direct_preferred,
         nhwc_into,
@@ -545,8 +560,13 @@ def main() -> None:
         else:
             L["mid"] = torch.empty((cfg.batch, cfg.h_in, cfg.w_in, nhwc_pitch(cfg.c_in, args.variant)), device=dev,
                                    dtype=torch.bfloat16 if args.variant == "bf16" else torch.float32)
-            L["tr"] = (lambda L=L: nhwc_into(L["x"], L["mid"]))
-            L["cv"] = (lambda L=L: conv_fused_into(L["mid"], L["f"], L["out"], L["cfg"].params, args.variant))
+            if cfg.params.pad:
+                L["tr"] = (lambda L=L: nhwc_into(L["x"], L["mid"]))
+                L["cv"] = (lambda L=L: conv_fused_into(L["mid"], L["f"], L["out"], L["cfg"].params, args.variant))
+            else:  # production one-call path: the channels-last copy is part of the conv call
+                L["tr"] = lambda: None
+                L["cv"] = (lambda L=L: conv_fused_nchw_into(L["x"], L["mid"], L["f"], L["out"], L["cfg"].params,
+                                                            args.variant))
         layers.append(L)
 
     def step():

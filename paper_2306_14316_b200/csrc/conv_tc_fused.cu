@@ -462,7 +462,7 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
                               : "conv_tc_fused_kernel (generic TMA window boxes, filter resident, tf32)")
                      : (BF16 ? "conv_tc_fused_kernel (generic TMA window boxes, bf16)"
                              : "conv_tc_fused_kernel (generic TMA window boxes, tf32)"));
-  e = launch_tc_kernel(kern, grid, smem, stream, feed.src != nullptr, 1, a, map_a, map_b, feed);
+  e = launch_tc_kernel(kern, grid, smem, stream, feed.src != nullptr, 1, a, map_a, map_b, feed_for(feed, grid, tiles));
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
@@ -513,7 +513,8 @@ int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c
     feed.chunks = static_cast<uint32_t>((h * w + pix - 1) / pix);
     feed.units_per_img = feed.chunks * ((feed.c_pad + grp - 1) / grp);
     feed.ready = counters;
-    feed.next = counters + n;
+    feed.front = counters + n;
+    feed.lookahead = 0xffffffffu;  // no conv to follow
     cudaMemsetAsync(counters, 0, (n + 1) * 4, stream);
     const int g = atoi(getenv("IM2WIN_FEED_PROBE"));  // CTAs of kFeedWarps warps
     if (bf16) nhwc_feed_only_kernel<true><<<g, 32 * kFeedWarps, 0, stream>>>(feed);
@@ -635,13 +636,15 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
     // In-kernel feed or a copy kernel first.  Measured (tools/feed_ab.py): the feed warps and the
     // conv share the memory system, so overlap pays only where the conv's own traffic is light
     // next to the input -- output/input elements r = (Co*Ho*Wo)/(C*H*W) <= 0.5 (strided layers:
-    // conv4 BF16 1.35 -> 0.97 ms, TF32 2.00 -> 1.82 ms at N=128); at r ~ 0.9 (conv9/10) it ties,
-    // and at r >= 1.4 (conv5/6/8) it loses up to 18%.  IM2WIN_FEED: 0 never, 1 auto, 2 always.
+    // conv4 BF16 1.22 -> 1.02 ms, TF32 2.15 -> 1.81-1.89 ms at N=128; 4.80 -> 4.06 and
+    // 8.43 -> 7.34 ms at N=512) -- and not at N=2048 (conv4 BF16 19.0 vs 20.0 ms, TF32 33.1 vs
+    // 32.4-33.5 at any lookahead); at r ~ 0.9 (conv9/10) it ties or loses, at r >= 1.4 (conv5/6/8)
+    // it loses up to 18%.  IM2WIN_FEED: 0 never, 1 auto (r <= 0.5 and N <= 512), 2 always.
     const char* fe = getenv("IM2WIN_FEED");
     const int mode = fe ? atoi(fe) : 1;
     const int64_t h_o = (h - h_f) / stride + 1, w_o = (w - w_f) / stride + 1;
     const double r = static_cast<double>(c_out * h_o * w_o) / static_cast<double>(c_in * h * w);
-    if (mode == 0 || (mode == 1 && r > 0.5)) {
+    if (mode == 0 || (mode == 1 && (r > 0.5 || n > 512))) {
       const int rc = im2win_launch_nchw_to_nhwc(feed_src, const_cast<void*>(x_cl), n, c_in, h, w, bf16, 0, stream, err);
       if (rc) return rc;
       feed_src = nullptr;
@@ -664,7 +667,8 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
     feed.chunks = static_cast<uint32_t>((hw + pix - 1) / pix);
     feed.units_per_img = feed.chunks * ((feed.c_pad + grp - 1) / grp);
     feed.ready = im2win_tc_feed_counters(workspace, c_in, c_out, h_f, w_f);
-    feed.next = feed.ready + n;
+    feed.front = feed.ready + n;
+    feed.lookahead = 2;  // set per kernel by the launcher (feed_lookahead)
     feed.nowait = getenv("IM2WIN_FEED_NOWAIT") && atoi(getenv("IM2WIN_FEED_NOWAIT")) ? 1u : 0u;
     cudaError_t e = cudaMemsetAsync(feed.ready, 0, static_cast<size_t>(n + 1) * 4, stream);
     if (e != cudaSuccess) {

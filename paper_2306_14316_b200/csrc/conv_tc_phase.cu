@@ -387,7 +387,7 @@ static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64
                                : "conv_tc_phase_kernel (phase shift, 2 tiles/item)");
   }
   e = launch_tc_kernel(kern, grid, smem, stream, feed.src != nullptr, PAIR ? 2 : 1, a, map_a[0], map_a[1], map_b,
-                       feed);
+                       feed_for(feed, PAIR ? grid / 2 : grid, items));
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
     return 2;

@@ -317,7 +317,7 @@ static int launch_shift(ShiftArgs a, const void* x_cl, const void* packed, int64
   const uint64_t tiles = static_cast<uint64_t>(a.n_tiles) * a.oh_tiles * a.ow_tiles * a.co_tiles;
   const uint32_t grid = tiles < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(tiles) : static_cast<uint32_t>(sms);
   im2win_note_kernel(RB ? "conv_tc_shift_kernel (window shift, filter resident)" : "conv_tc_shift_kernel (window shift)");
-  e = launch_tc_kernel(kern, grid, smem, stream, feed.src != nullptr, 1, a, map_a, map_b, feed);
+  e = launch_tc_kernel(kern, grid, smem, stream, feed.src != nullptr, 1, a, map_a, map_b, feed_for(feed, grid, tiles));
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
     return 2;

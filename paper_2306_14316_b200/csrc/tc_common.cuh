@@ -6,6 +6,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <utility>
 
@@ -202,9 +203,23 @@ struct NhwcFeed {
   uint32_t chunks;         // ceil(hw / kPix)
   uint32_t units_per_img;  // chunks * ceil(c_pad / G)
   uint32_t* ready;         // [n_img] finished units per image
-  uint32_t* next;          // unit claim counter
+  uint32_t* front;         // highest image any TMA producer has started a tile of
+  uint32_t lookahead;      // the feed converts image i only once front >= i - lookahead
   uint32_t nowait;         // A/B probe only (IM2WIN_FEED_NOWAIT): the producer does not wait
 };
+
+// Throttle: keep the channels-last copy at most `lookahead` images ahead of the conv, so the
+// bytes the feed writes are still in L2 when the TMA engine reads them (a feed running far
+// ahead pushes its copy to HBM and competes with the conv for bandwidth).  lookahead is at
+// least one grid-round of images (set by the launcher), so no producer waits on a throttled unit.
+IM2WIN_DEVICE void feed_throttle(const NhwcFeed& f, uint32_t img) {
+  for (;;) {
+    uint32_t fr;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(fr) : "l"(f.front) : "memory");
+    if (img <= fr || img - fr <= f.lookahead) return;
+    __nanosleep(256);
+  }
+}
 
 IM2WIN_DEVICE void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
 
@@ -280,43 +295,59 @@ IM2WIN_DEVICE void nhwc_feed_run(const NhwcFeed& f, int lane, uint32_t feed_warp
   const uint32_t total = f.n_img * f.units_per_img;
   // this warp's units: blocks of kFeedBatch consecutive units, every feed_warps-th block
   auto step = [&](uint32_t u) { return (u + 1) % kFeedBatch ? u + 1 : u + 1 + (feed_warps - 1) * kFeedBatch; };
+  auto may_load = [&](uint32_t u) {  // the throttle would not hold unit u back
+    uint32_t fr;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(fr) : "l"(f.front) : "memory");
+    const uint32_t img = u / f.units_per_img;
+    return img <= fr || img - fr <= f.lookahead;
+  };
   float va[S::J][S::G], vb[S::J][S::G];
   uint32_t pend_img = 0, pend = 0;
-  uint32_t ua = feed_warp * kFeedBatch;
-  if (ua < total) feed_load<BF16>(f, ua, lane, va);
-  while (ua < total) {
-    const uint32_t ub = step(ua);
-    if (ub < total) feed_load<BF16>(f, ub, lane, vb);
-    const uint32_t img = ua / f.units_per_img;
-    if (pend && img != pend_img) {
-      feed_publish(f, pend_img, pend, lane);
-      pend = 0;
-    }
-    feed_store<BF16>(f, ua, lane, va);
+  auto publish = [&]() {
+    if (pend) feed_publish(f, pend_img, pend, lane);
+    pend = 0;
+  };
+  // store unit u (data v) and account for it; publish at image changes and block ends
+  auto finish = [&](uint32_t u, uint32_t next, const float(&v)[S::J][S::G]) {
+    const uint32_t img = u / f.units_per_img;
+    if (pend && img != pend_img) publish();
+    feed_store<BF16>(f, u, lane, v);
     pend_img = img;
     ++pend;
-    if (ub != ua + 1 && pend) {  // end of a block
-      feed_publish(f, pend_img, pend, lane);
-      pend = 0;
-    }
+    if (next != u + 1) publish();
+  };
+  // The next unit's loads are issued before the current unit is stored -- unless the throttle
+  // would hold it: then the current unit is stored and published first (the conv may be
+  // waiting for it), and only then does the warp wait.
+  uint32_t ua = feed_warp * kFeedBatch;
+  if (ua < total) {
+    feed_throttle(f, ua / f.units_per_img);
+    feed_load<BF16>(f, ua, lane, va);
+  }
+  while (ua < total) {
+    const uint32_t ub = step(ua);
+    bool pre = ub < total && may_load(ub);
+    if (pre) feed_load<BF16>(f, ub, lane, vb);
+    finish(ua, ub, va);
     if (ub >= total) break;
-    const uint32_t imgb = ub / f.units_per_img;
-    const uint32_t uc = step(ub);
-    if (uc < total) feed_load<BF16>(f, uc, lane, va);
-    if (pend && imgb != pend_img) {
-      feed_publish(f, pend_img, pend, lane);
-      pend = 0;
+    if (!pre) {
+      publish();
+      feed_throttle(f, ub / f.units_per_img);
+      feed_load<BF16>(f, ub, lane, vb);
     }
-    feed_store<BF16>(f, ub, lane, vb);
-    pend_img = imgb;
-    ++pend;
-    if (uc != ub + 1 && pend) {
-      feed_publish(f, pend_img, pend, lane);
-      pend = 0;
+    const uint32_t uc = step(ub);
+    pre = uc < total && may_load(uc);
+    if (pre) feed_load<BF16>(f, uc, lane, va);
+    finish(ub, uc, vb);
+    if (uc >= total) break;
+    if (!pre) {
+      publish();
+      feed_throttle(f, uc / f.units_per_img);
+      feed_load<BF16>(f, uc, lane, va);
     }
     ua = uc;
   }
-  if (pend) feed_publish(f, pend_img, pend, lane);
+  publish();
 }
 
 // Producer side: block until images [lo, hi] are complete.  [conf_lo, conf_hi] caches the
@@ -325,6 +356,8 @@ IM2WIN_DEVICE void nhwc_feed_wait(const NhwcFeed& f, uint32_t lo, uint32_t hi, u
                                   uint32_t& conf_hi) {
   if (f.src == nullptr || f.nowait) return;
   if (hi >= f.n_img) hi = f.n_img - 1;
+  // publish the conv front (the feed's throttle); once per new highest image
+  if (!(conf_lo <= conf_hi && hi <= conf_hi)) atomicMax(f.front, hi);
   bool waited = false;
   for (uint32_t i = lo; i <= hi; ++i) {
     if (i >= conf_lo && i <= conf_hi) continue;
@@ -339,6 +372,19 @@ IM2WIN_DEVICE void nhwc_feed_wait(const NhwcFeed& f, uint32_t lo, uint32_t hi, u
     else { conf_lo = i; conf_hi = i; }
   }
   if (waited) fence_proxy_async_global();
+}
+
+// Feed lookahead for a persistent grid walking `items` work items over n_img images in image
+// order: one grid-round of images plus two (the producers of a round never wait on a throttled unit).
+inline NhwcFeed feed_for(const NhwcFeed& f, uint64_t grid, uint64_t items) {
+  NhwcFeed g = f;
+  // IM2WIN_FEED_ROUNDS: lookahead in grid-rounds (A/B; 0 = unthrottled)
+  static const int rounds = getenv("IM2WIN_FEED_ROUNDS") ? atoi(getenv("IM2WIN_FEED_ROUNDS")) : 0;
+  if (g.src && items) {
+    g.lookahead = rounds <= 0 ? 0xffffffffu
+                              : static_cast<uint32_t>(rounds * ((grid * g.n_img + items - 1) / items) + 2);
+  }
+  return g;
 }
 
 // Launch of a TMA-fed conv kernel: with a feed, the extra converter warps and a cooperative

@@ -835,3 +835,21 @@ def test_tc_phase_cta_pair(variant, layer_goldens, monkeypatch):
         seen.add(_lib.last_kernel())
         assert pkg.normalized_max_diff(out, orc.conv_direct(inp, flt, s)) <= TC_TOL[variant], (n, c, h, w)
     assert any("CTA pair" in k for k in seen), seen
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_captured_conv_with_feed(variant, monkeypatch):
+    """CapturedConv records the one-call fused path with the in-kernel feed (a cooperative
+    launch plus the counter memset) and replays it bit-identically to the eager call."""
+    monkeypatch.setenv("IM2WIN_FEED", "2")
+    params = pkg.ConvParams(64, 64, 7, 7, 2)
+    g = torch.Generator(device=DEV).manual_seed(3)
+    x = torch.randn((3, 64, 40, 44), device=DEV, generator=g)
+    f = torch.randn((64, 64, 7, 7), device=DEV, generator=g)
+    cc = pkg.CapturedConv(x.shape, params, f, variant=variant)
+    eager = pkg.conv_im2win_opt(x, f, params, variant=variant).numpy()
+    for _ in range(2):
+        got = cc(x).numpy()
+        assert bits_equal(got, eager)
+    x2 = torch.randn_like(x)
+    assert bits_equal(cc(x2).numpy(), pkg.conv_im2win_opt(x2, f, params, variant=variant).numpy())
