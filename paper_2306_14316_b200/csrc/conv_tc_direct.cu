@@ -267,27 +267,42 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
       auto build_slab = [&](uint32_t sl, auto check) {
         const uint32_t arow = smem_u32(a_ring + stage * kATile) + arow_i * kRowBytes;
         const uint32_t ko = koff_s + 4 * sl * kBK;
+        // chunks in groups of CG: per group three latency levels (the loads are volatile asm,
+        // issued in program order) -- every chunk's window offsets (warp-uniform: broadcast
+        // loads), then every gather, then the packs and stores.  Measured (tools/direct_ab.py,
+        // N=128): TF32 all 4 chunks at once +6-10% over chunk by chunk; BF16 (8 values per
+        // chunk) 4 at once -4%, 2 at once -3%, so it stays chunk by chunk.
+        constexpr int CG = BF16 ? 1 : kChunksPerThread;
 #pragma unroll
-        for (int jj = 0; jj < kChunksPerThread; ++jj) {
-          const int j = kChunksPerThread * half + jj;
-          // this chunk's kPerChunk window offsets (warp-uniform: broadcast loads)
-          int off[8];
-          const int4 o_lo = lds128i(ko + 4 * (j * kPerChunk));
-          off[0] = o_lo.x; off[1] = o_lo.y; off[2] = o_lo.z; off[3] = o_lo.w;
-          if constexpr (BF16) {
-            const int4 o_hi = lds128i(ko + 4 * (j * kPerChunk + 4));
-            off[4] = o_hi.x; off[5] = o_hi.y; off[6] = o_hi.z; off[7] = o_hi.w;
+        for (int jg = 0; jg < kChunksPerThread; jg += CG) {
+          int off[CG][8];
+#pragma unroll
+          for (int jj = 0; jj < CG; ++jj) {
+            const int j = kChunksPerThread * half + jg + jj;
+            const int4 o_lo = lds128i(ko + 4 * (j * kPerChunk));
+            off[jj][0] = o_lo.x; off[jj][1] = o_lo.y; off[jj][2] = o_lo.z; off[jj][3] = o_lo.w;
+            if constexpr (BF16) {
+              const int4 o_hi = lds128i(ko + 4 * (j * kPerChunk + 4));
+              off[jj][4] = o_hi.x; off[jj][5] = o_hi.y; off[jj][6] = o_hi.z; off[jj][7] = o_hi.w;
+            }
           }
-          float v[kPerChunk];
+          float v[CG][kPerChunk];
 #pragma unroll
-          for (int e = 0; e < kPerChunk; ++e) {
-            if constexpr (decltype(check)::value) v[e] = off[e] >= 0 ? lds32(my_base + 4 * off[e]) : 0.0f;
-            else v[e] = lds32(my_base + 4 * off[e]);
+          for (int jj = 0; jj < CG; ++jj)
+#pragma unroll
+            for (int e = 0; e < kPerChunk; ++e) {
+              if constexpr (decltype(check)::value) v[jj][e] = off[jj][e] >= 0 ? lds32(my_base + 4 * off[jj][e]) : 0.0f;
+              else v[jj][e] = lds32(my_base + 4 * off[jj][e]);
+            }
+#pragma unroll
+          for (int jj = 0; jj < CG; ++jj) {
+            const int j = kChunksPerThread * half + jg + jj;
+            uint32_t w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              w[q] = BF16 ? pack_bf16x2(v[jj][2 * q], v[jj][(2 * q + 1) % kPerChunk]) : to_tf32(v[jj][q]);
+            sts128(arow + ((j ^ (arow_i & 7)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
           }
-          uint32_t w[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) w[q] = BF16 ? pack_bf16x2(v[2 * q], v[(2 * q + 1) % kPerChunk]) : to_tf32(v[q]);
-          sts128(arow + ((j ^ (arow_i & 7)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
         }
       };
       for (uint32_t sl = 0; sl < a.slabs; ++sl) {

@@ -39,7 +39,7 @@ if "--child" in sys.argv:
 else:
     libs = [a for a in sys.argv[1:] if not a.startswith("--")]
     layers = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--layers=")), "conv1,conv2,conv3,conv7")
-    for rnd in range(2):
+    for rnd in range(int(os.environ.get("AB_ROUNDS", "2"))):
         for lib in libs:
             env = dict(os.environ, IM2WIN_LIB=str(Path(lib).resolve()))
             r = subprocess.run([sys.executable, __file__, "--child", layers], env=env, capture_output=True, text=True)
