@@ -12,6 +12,8 @@ Extra keyword `variant` (default "fp32-exact") selects the arithmetic:
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -324,7 +326,44 @@ def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, 
         fd = f.data if f.device == i.device else f.data.to(i.device)
         conv_cl_into(win_cl, fd, out, params, variant)
         return Tensor4(out)
-    return compute_from_windows_opt(im2win(i, params), f, params, plan, variant=variant)
+    return _fp32_chunked(i, f, params, plan, variant, h_out, w_out)
+
+
+def window_budget_bytes() -> int:
+    """Largest im2win tensor conv_im2win_opt materialises at once (FP32 variants); larger
+    batches are transformed and convolved in image chunks through one reused Ĩ buffer.
+    IM2WIN_WINDOW_BUDGET (bytes; 0 = no limit), default 1 GiB."""
+    return int(os.environ.get("IM2WIN_WINDOW_BUDGET", str(1 << 30)))
+
+
+def _fp32_chunked(i: Tensor4, f: Tensor4, params: ConvParams, plan, variant: str, h_out: int,
+                  w_out: int) -> Tensor4:
+    """Transform + tiled conv; with Ĩ above the window budget, in image chunks.
+
+    Images are independent (reference.py:78-90, the GEMM columns of different images never
+    mix), so a chunk's transform + conv writes exactly the output rows the full-batch call
+    would, with the same bits.  Peak extra memory: one chunk's Ĩ instead of the batch's
+    (conv4 at N=128: 1.0 GB instead of 5.6 GB).  A chunk is at least 8 images so the conv
+    grid still fills the GPU.
+    """
+    from .layouts import effective_width, im2win_into
+
+    n_img = i.dims[0]
+    w_eff = effective_width(w_out, params.w_f, params.stride)
+    per_img = params.c_in * h_out * params.h_f * w_eff * 4
+    budget = window_budget_bytes()
+    if budget <= 0 or per_img * n_img <= budget:
+        return compute_from_windows_opt(im2win(i, params), f, params, plan, variant=variant)
+    chunk = max(8, budget // per_img)
+    fd = f.data if f.device == i.device else f.data.to(i.device)
+    out = torch.empty((n_img, params.c_out, h_out, w_out), dtype=DTYPE, device=i.device)
+    win = torch.empty((min(chunk, n_img), params.c_in, h_out, params.h_f * w_eff), dtype=DTYPE, device=i.device)
+    for lo in range(0, n_img, chunk):
+        hi = min(n_img, lo + chunk)
+        wv = win[: hi - lo]
+        im2win_into(i.data[lo:hi], wv, params)
+        conv_windows_into(wv, fd, out[lo:hi], params, w_eff, plan, variant)
+    return Tensor4(out)
 
 
 def _host_f32(x, ndim: int) -> torch.Tensor:

@@ -853,3 +853,34 @@ def test_captured_conv_with_feed(variant, monkeypatch):
         assert bits_equal(got, eager)
     x2 = torch.randn_like(x)
     assert bits_equal(cc(x2).numpy(), pkg.conv_im2win_opt(x2, f, params, variant=variant).numpy())
+
+
+@pytest.mark.parametrize("variant", ["fp32-exact", "fp32-fma"])
+def test_fp32_window_budget_chunks_bitwise(variant, monkeypatch, layer_goldens):
+    """With Ĩ above the window budget conv_im2win_opt transforms and convolves image chunks
+    through one reused Ĩ buffer: same bits as the full-batch call (ragged last chunk, padding),
+    and the reference goldens still match."""
+    for name, n in (("conv9", 19), ("conv3", 9), ("conv12", 17)):
+        cfg = replace(BENCHMARKS[name], batch=n, seed=5)
+        inp, flt = make_inputs(cfg)
+        x = torch.from_numpy(inp).to(DEV)
+        monkeypatch.setenv("IM2WIN_WINDOW_BUDGET", "0")
+        full = pkg.conv_im2win_opt(x, flt, cfg.params, variant=variant).numpy()
+        monkeypatch.setenv("IM2WIN_WINDOW_BUDGET", "1")  # forces chunks of 8 images
+        chunked = pkg.conv_im2win_opt(x, flt, cfg.params, variant=variant).numpy()
+        assert bits_equal(chunked, full), name
+    monkeypatch.setenv("IM2WIN_WINDOW_BUDGET", "1")
+    params = pkg.ConvParams(3, 8, 3, 3, 1, pad=1)
+    rng = np.random.default_rng(2)
+    inp = rng.standard_normal((11, 3, 13, 10), dtype=np.float32)
+    flt = rng.standard_normal((8, 3, 3, 3), dtype=np.float32)
+    chunked = pkg.conv_im2win_opt(inp, flt, params, variant=variant).numpy()
+    monkeypatch.setenv("IM2WIN_WINDOW_BUDGET", "0")
+    assert bits_equal(chunked, pkg.conv_im2win_opt(inp, flt, params, variant=variant).numpy())
+    if variant == "fp32-exact":
+        g = layer_goldens["conv9"]
+        cfg = replace(BENCHMARKS["conv9"], batch=g["batch"], seed=g["seed"])
+        inp, flt = make_inputs(cfg)
+        monkeypatch.setenv("IM2WIN_WINDOW_BUDGET", "1")
+        out = pkg.conv_im2win_opt(inp, flt, cfg.params).numpy()
+        assert orc.checksum(out) == g["out_sha"]
