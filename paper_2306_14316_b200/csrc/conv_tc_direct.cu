@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kDirThreads, 1) conv_tc_direct_kernel(const Di
         if (valid) {
 #pragma unroll
           for (int q = 0; q < 16; ++q)
-            if (j0 + q < static_cast<int>(a.co)) a.out[obase + static_cast<int64_t>(j0 + q) * a.hw] = __uint_as_float(v[q]);
+            if (j0 + q < static_cast<int>(a.co)) st_out(a.out + obase + static_cast<int64_t>(j0 + q) * a.hw, __uint_as_float(v[q]));
         }
       }
       tc_fence_before();

@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
         if (valid) {
 #pragma unroll
           for (int q = 0; q < 16; ++q)
-            if (m0 + q < a.co) a.out[obase + static_cast<int64_t>(m0 + q) * a.hw] = __uint_as_float(v[q]);
+            if (m0 + q < a.co) st_out(a.out + obase + static_cast<int64_t>(m0 + q) * a.hw, __uint_as_float(v[q]));
         }
       }
       tc_fence_before();

@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
           if (m0 + q < a.co) {
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
-              if (valid[mt]) a.out[obase[mt] + static_cast<int64_t>(m0 + q) * a.hw] = __uint_as_float(v[mt][q]);
+              if (valid[mt]) st_out(a.out + obase[mt] + static_cast<int64_t>(m0 + q) * a.hw, __uint_as_float(v[mt][q]));
           }
         }
 #else

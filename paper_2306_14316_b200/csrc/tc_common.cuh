@@ -153,6 +153,32 @@ IM2WIN_DEVICE void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+// Output store of the TC epilogues (lane = pixel: one 128-byte piece of a channel plane per warp
+// instruction).  IM2WIN_ST_MODE (build flag, A/B with tools/lib_ab.py): 0 plain st.global,
+// 1 st.global.cs (streaming; default), 2 L2::evict_last policy, 3 L2::evict_first policy,
+// 4 st.global.wt.  Measured (N=128, production path): .cs +1-4% on conv9/conv10 BF16, else
+// within 1%; evict_last +5% on conv7 but -10% on conv8 BF16; evict_first -1..-10%.
+#ifndef IM2WIN_ST_MODE
+#define IM2WIN_ST_MODE 1
+#endif
+IM2WIN_DEVICE void st_out(float* p, float v) {
+#if IM2WIN_ST_MODE == 1
+  __stcs(p, v);
+#elif IM2WIN_ST_MODE == 2 || IM2WIN_ST_MODE == 3
+  uint64_t pol;
+#if IM2WIN_ST_MODE == 2
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+#else
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+#endif
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;\n" ::"l"(p), "f"(v), "l"(pol) : "memory");
+#elif IM2WIN_ST_MODE == 4
+  __stwt(p, v);
+#else
+  *p = v;
+#endif
+}
+
 IM2WIN_DEVICE uint32_t to_tf32(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
