@@ -31,6 +31,26 @@ for (n, c, h, w, co, hf, wf, s, p) in cases:
                 continue
             pkg.conv_im2win_opt(x, f, params, variant=v, tc_path=path)
     pkg.conv_im2win_opt_host(x.cpu(), f.cpu(), params, chunk_images=1)
+# round 2: the in-kernel channels-last feed (forced on every TMA-fed kernel), CTA pairs, the
+# FP32 window-budget chunks
+import os  # noqa: E402
+
+for (n, c, h, w, co, hf, wf, s, p) in cases:
+    if p:
+        continue
+    x = torch.from_numpy(rng.standard_normal((n + 2, c, h, w), dtype=np.float32)).cuda()
+    f = torch.from_numpy(rng.standard_normal((co, c, hf, wf), dtype=np.float32)).cuda()
+    params = pkg.ConvParams(c, co, hf, wf, s)
+    for env in ({"IM2WIN_FEED": "2"}, {"IM2WIN_FEED": "2", "IM2WIN_FEED_ROUNDS": "1"},
+                {"IM2WIN_FEED": "2", "IM2WIN_PAIR": "1", "IM2WIN_PHASE": "2"}):
+        os.environ.update(env)
+        for v in ("tf32", "bf16"):
+            pkg.conv_im2win_opt(x, f, params, variant=v, tc_path="fused")
+        for k in env:
+            del os.environ[k]
+    os.environ["IM2WIN_WINDOW_BUDGET"] = "1"
+    pkg.conv_im2win_opt(torch.cat([x] * 5), f, params)
+    del os.environ["IM2WIN_WINDOW_BUDGET"]
 # 4-byte-offset operands (the staged transform aligns its 16-byte copies to the address)
 for (n, c, h, w, co, hf, wf, s, p) in cases[:3]:
     base = torch.from_numpy(rng.standard_normal(1 + n * c * h * w, dtype=np.float32)).cuda()
