@@ -703,9 +703,11 @@ def main() -> None:
     # ---- tensor-core legs of BASELINE configs 4 and 5 (all ranks; max over ranks) ----
     if not args.no_tc:
         tc = {"tolerance": {"tf32": "max|d|/rms(ref) <= 1e-2", "bf16": "max|d|/rms(ref) <= 4e-2"},
-              "note": "production path (direct kernel, or NHWC copy + fused/shift/phase kernel); s = transform+conv "
-                      "per call, max over ranks; roofline = min(tensor peak, AI x HBM) with AI on the minimal "
-                      "bytes (NCHW f32 in + filter + NCHW f32 out)"}
+              "note": "production path (direct kernel, or the one-call im2win_conv_fused_nchw: channels-last copy "
+                      "inside the conv kernel or by the copy kernel first, then the fused/shift/phase kernel); "
+                      "s = the whole call, conv_s = the conv kernel alone on an existing copy; max over ranks; "
+                      "roofline = min(tensor peak, AI x HBM) with AI on the minimal bytes (NCHW f32 in + filter + "
+                      "NCHW f32 out)"}
         for v in ("tf32", "bf16"):
             traffic = load_tc_traffic(v)
             tc[v] = {}
