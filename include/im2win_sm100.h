@@ -89,6 +89,17 @@ int im2win_conv_f32(const float* windows, const float* flt, float* out, int64_t 
                     int32_t w_f, int32_t stride, const im2win_tile_plan* plan, int32_t variant,
                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* The FP32 conv_im2win_opt without a materialised Ĩ (replaces the transform + _tiled_kernel
+ * pair of pkg/src/winconv/kernels/optimized.py:237-241 in one launch): the same kernels gather
+ * every window element Ĩ[img][c][oh][(ow*s + fw)*Hf + fh] = x[img][c][oh*s + fh][ow*s + fw]
+ * straight from the NCHW input x (n, c_in, h, w), in the reference's k order -- bit-identical
+ * to im2win_transform_f32 + im2win_conv_f32.  variant = IM2WIN_FP32_EXACT or IM2WIN_FP32_FMA;
+ * plan as for im2win_conv_f32 (micro_kernel must be 1); workspace as im2win_conv_workspace_bytes. */
+int im2win_conv_nchw_f32(const float* x, const float* flt, float* out, int64_t n, int64_t c_in,
+                         int64_t h, int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
+                         const im2win_tile_plan* plan, int32_t variant, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
 /* Paper Alg. 2 basic kernel: one output per thread, operands from global memory
  * (replaces _basic_window_kernel, kernels/reference.py:180-206, called at :215).
  * Bit-exact like im2win_conv_f32 with IM2WIN_FP32_EXACT. */

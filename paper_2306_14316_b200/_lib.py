@@ -29,6 +29,7 @@ EXPORTED_SYMBOLS = (
     "im2win_transform_f32_padded",
     "im2win_conv_workspace_bytes",
     "im2win_conv_f32",
+    "im2win_conv_nchw_f32",
     "im2win_last_error",
     "im2win_last_kernel",
     "im2win_conv_launch_count",
@@ -92,6 +93,9 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         lib.im2win_conv_f32.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i32, i32, i32,
                                         ctypes.POINTER(TilePlanC), i32, vp, sz, vp]
         lib.im2win_conv_f32.restype = ctypes.c_int
+        lib.im2win_conv_nchw_f32.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i32, i32, i32,
+                                             ctypes.POINTER(TilePlanC), i32, vp, sz, vp]
+        lib.im2win_conv_nchw_f32.restype = ctypes.c_int
         lib.im2win_last_error.argtypes = []
         lib.im2win_last_error.restype = ctypes.c_char_p
         lib.im2win_last_kernel.argtypes = []

@@ -13,7 +13,8 @@ int im2win_launch_transform(const float* src, float* dst, int64_t n, int64_t c, 
 int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void* workspace,
                             int64_t n, int64_t c_in, int64_t c_out, int64_t h_out, int64_t w_out,
                             int64_t row_len, int h_f, int w_f, int stride, int cfg, int exact,
-                            int vec, int stages, cudaStream_t stream, const char** err);
+                            int vec, int stages, cudaStream_t stream, const char** err,
+                            const int64_t* nchw_hw = nullptr);
 int im2win_launch_conv_simt_1x1(const float* win, const float* flt, float* out, void* workspace,
                                 int64_t n, int64_t c_in, int64_t c_out, int64_t h_out,
                                 int64_t w_out, int64_t row_len, int h_f, int w_f, int stride,
@@ -139,6 +140,33 @@ int im2win_conv_f32(const float* windows, const float* flt, float* out, int64_t 
     default:
       return fail(1, "im2win_conv_f32: unknown variant");
   }
+  return rc ? fail(rc, err) : 0;
+}
+
+int im2win_conv_nchw_f32(const float* x, const float* flt, float* out, int64_t n, int64_t c_in, int64_t h,
+                         int64_t w, int64_t c_out, int32_t h_f, int32_t w_f, int32_t stride,
+                         const im2win_tile_plan* plan, int32_t variant, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+  g_last_error[0] = '\0';
+  if (!x || !flt || !out) return fail(1, "im2win_conv_nchw_f32: null pointer");
+  if (n < 1 || c_in < 1 || c_out < 1 || h < 1 || w < 1 || h_f < 1 || w_f < 1 || stride < 1)
+    return fail(1, "im2win_conv_nchw_f32: extents must be positive");
+  if (h_f > h || w_f > w) return fail(1, "im2win_conv_nchw_f32: filter larger than input");
+  if (variant != IM2WIN_FP32_EXACT && variant != IM2WIN_FP32_FMA)
+    return fail(1, "im2win_conv_nchw_f32: variant must be IM2WIN_FP32_EXACT or IM2WIN_FP32_FMA");
+  if (workspace_bytes < im2win_conv_workspace_bytes(c_in, c_out, h_f, w_f, variant) || !workspace)
+    return fail(1, "im2win_conv_nchw_f32: workspace too small");
+  im2win_tile_plan def = {-1, 1, 1, 1};
+  const im2win_tile_plan* p = plan ? plan : &def;
+  if (!p->micro_kernel) return fail(1, "im2win_conv_nchw_f32: micro_kernel=False is an ablation of the Ĩ path");
+  if (int rc = bind_device_of(out)) return rc;
+  const int64_t h_out = (h - h_f) / stride + 1, w_out = (w - w_f) / stride + 1;
+  const int64_t hw[2] = {h, w};
+  const char* err = nullptr;
+  const int rc = im2win_launch_conv_simt(x, flt, out, workspace, n, c_in, c_out, h_out, w_out, 0, h_f, w_f, stride,
+                                         p->block_cfg, variant == IM2WIN_FP32_EXACT, p->vectorized_load,
+                                         p->prefetch_double_buffer ? 3 : 1, static_cast<cudaStream_t>(stream), &err,
+                                         hw);
   return rc ? fail(rc, err) : 0;
 }
 

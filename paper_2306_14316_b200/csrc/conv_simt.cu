@@ -63,6 +63,10 @@ struct ConvArgs {
   int M, Mp, K, Kp;
   uint32_t n_gemm;                  // N*Ho*Wo
   uint32_t c_in, h_out, w_out, row_len, s_hf, hw;
+  // GEMM column n = (img, oh, ow) starts at img*img_stride + oh*row_stride + ow*col_stride in the
+  // source: the im2win tensor Ĩ (c_in*h_out*row_len, row_len, s*Hf) or, for the no-Ĩ entry point,
+  // the NCHW input itself (C*H*W, s*W, s) -- the same window elements, so the same bits
+  uint32_t img_stride, row_stride, col_stride;
   FastDiv fd_hw, fd_wo;
   uint32_t m_tiles;
   uint32_t vec_out;                 // Ho*Wo % 4 == 0: 16-byte output stores
@@ -70,11 +74,12 @@ struct ConvArgs {
 };
 
 // ---------------------------------------------------------------------------
-// pack: FT[k][m] = F[m][k] (zero padded), delta[k] = c*Ho*RL + fw*Hf + fh
+// pack: FT[k][m] = F[m][k] (zero padded), delta[k] = c*chan_stride + fh*fh_stride + fw*fw_stride
+// (Ĩ: c*Ho*RL + fw*Hf + fh; NCHW input: c*H*W + fh*W + fw)
 // ---------------------------------------------------------------------------
 __global__ void pack_filter_kernel(const float* __restrict__ flt, float* __restrict__ fltT,
                                    int* __restrict__ delta, int M, int K, int Mp, int Kp, int h_f,
-                                   int w_f, int chan_stride) {
+                                   int w_f, int chan_stride, int fh_stride, int fw_stride) {
   const int64_t total = static_cast<int64_t>(Kp) * Mp;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -87,7 +92,7 @@ __global__ void pack_filter_kernel(const float* __restrict__ flt, float* __restr
         int fhw = h_f * w_f;
         int c = k / fhw, r = k % fhw;
         int fh = r / w_f, fw = r % w_f;
-        d = c * chan_stride + fw * h_f + fh;
+        d = c * chan_stride + fh * fh_stride + fw * fw_stride;
       }
       delta[k] = d;
     }
@@ -152,8 +157,8 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? ((BM / MT) * 
       uint32_t img, rem, oh, ow;
       a.fd_hw.divmod(n, img, rem);
       a.fd_wo.divmod(rem, oh, ow);
-      bsrc[j] = a.win + (static_cast<int64_t>(img) * a.c_in * a.h_out + oh) * a.row_len +
-                static_cast<int64_t>(ow) * a.s_hf;
+      bsrc[j] = a.win + static_cast<int64_t>(img) * a.img_stride + static_cast<int64_t>(oh) * a.row_stride +
+                static_cast<int64_t>(ow) * a.col_stride;
       bzero[j] = false;
     }
   }
@@ -383,7 +388,8 @@ __global__ void __launch_bounds__(256, 2) conv_simt_smallk_kernel(const ConvArgs
       uint32_t img, rem, oh, ow;
       a.fd_hw.divmod(n, img, rem);
       a.fd_wo.divmod(rem, oh, ow);
-      src = a.win + (static_cast<int64_t>(img) * a.c_in * a.h_out + oh) * a.row_len + static_cast<int64_t>(ow) * a.s_hf;
+      src = a.win + static_cast<int64_t>(img) * a.img_stride + static_cast<int64_t>(oh) * a.row_stride +
+            static_cast<int64_t>(ow) * a.col_stride;
       zero = false;
     }
     float* dst = Bs + b * KP * BN + tid;
@@ -545,15 +551,21 @@ static const int kBM[kNumCfg] = {128, 64, 96, 128, 64, 128, 32};
 static const int kBKc[kNumCfg] = {16, 16, 16, 16, 16, 16, 16};
 static const int kMaxBK = 32;
 
+// nchw_hw == nullptr: `win` is the im2win tensor Ĩ (row_len = Hf * w_eff).  Otherwise `win` is the
+// NCHW input itself, nchw_hw = {H, W} (row_len unused): the kernels gather the same window
+// elements straight from it -- Ĩ[img][c][oh][(ow*s + fw)*Hf + fh] == X[img][c][oh*s + fh][ow*s + fw]
+// (layouts.py:73-83) -- so the results are bit-identical and Ĩ is never written.
 int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void* workspace,
                             int64_t n, int64_t c_in, int64_t c_out, int64_t h_out, int64_t w_out,
                             int64_t row_len, int h_f, int w_f, int stride, int cfg, int exact,
-                            int vec, int stages, cudaStream_t stream, const char** err) {
+                            int vec, int stages, cudaStream_t stream, const char** err,
+                            const int64_t* nchw_hw = nullptr) {
   using namespace im2win;
   const int64_t K = c_in * h_f * w_f;
   const int64_t hw = h_out * w_out;
   const int64_t n_gemm = n * hw;
-  if (n_gemm >= (1ll << 31) || K >= (1ll << 24) || c_in * h_out * row_len >= (1ll << 31)) {
+  const int64_t img_elems = nchw_hw ? c_in * nchw_hw[0] * nchw_hw[1] : c_in * h_out * row_len;
+  if (n_gemm >= (1ll << 31) || K >= (1ll << 24) || img_elems >= (1ll << 31)) {
     *err = "im2win_conv_f32: extents exceed the kernel's index range";
     return 1;
   }
@@ -574,10 +586,18 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
   float* fltT = static_cast<float*>(workspace);
   int* delta = reinterpret_cast<int*>(fltT + static_cast<int64_t>(Kp) * Mp);
 
-  pack_filter_kernel<<<256, 256, 0, stream>>>(flt, fltT, delta, static_cast<int>(c_out), static_cast<int>(K), Mp,
-                                              Kp, h_f, w_f, static_cast<int>(h_out * row_len));
+  if (nchw_hw)
+    pack_filter_kernel<<<256, 256, 0, stream>>>(flt, fltT, delta, static_cast<int>(c_out), static_cast<int>(K), Mp,
+                                                Kp, h_f, w_f, static_cast<int>(nchw_hw[0] * nchw_hw[1]),
+                                                static_cast<int>(nchw_hw[1]), 1);
+  else
+    pack_filter_kernel<<<256, 256, 0, stream>>>(flt, fltT, delta, static_cast<int>(c_out), static_cast<int>(K), Mp,
+                                                Kp, h_f, w_f, static_cast<int>(h_out * row_len), 1, h_f);
   ConvArgs a{};
   a.win = win;
+  a.img_stride = static_cast<uint32_t>(img_elems);
+  a.row_stride = static_cast<uint32_t>(nchw_hw ? stride * nchw_hw[1] : row_len);
+  a.col_stride = static_cast<uint32_t>(nchw_hw ? stride : stride * h_f);
   a.fltT = fltT;
   a.delta = delta;
   a.out = out;
@@ -714,7 +734,8 @@ __global__ void __launch_bounds__(256) conv_simt_1x1_kernel(const ConvArgs a) {
       uint32_t img, rem, oh, ow;
       a.fd_hw.divmod(n, img, rem);
       a.fd_wo.divmod(rem, oh, ow);
-      off = (static_cast<int64_t>(img) * a.c_in * a.h_out + oh) * a.row_len + static_cast<int64_t>(ow) * a.s_hf;
+      off = static_cast<int64_t>(img) * a.img_stride + static_cast<int64_t>(oh) * a.row_stride +
+            static_cast<int64_t>(ow) * a.col_stride;
     }
     col_off[tid] = off;
   }
@@ -789,9 +810,12 @@ int im2win_launch_conv_simt_1x1(const float* win, const float* flt, float* out, 
   float* fltT = static_cast<float*>(workspace);
   int* delta = reinterpret_cast<int*>(fltT + static_cast<int64_t>(Kp) * Mp);
   pack_filter_kernel<<<256, 256, 0, stream>>>(flt, fltT, delta, static_cast<int>(c_out), static_cast<int>(K), Mp,
-                                              Kp, h_f, w_f, static_cast<int>(h_out * row_len));
+                                              Kp, h_f, w_f, static_cast<int>(h_out * row_len), 1, h_f);
   ConvArgs a{};
   a.win = win; a.fltT = fltT; a.delta = delta; a.out = out;
+  a.img_stride = static_cast<uint32_t>(c_in * h_out * row_len);
+  a.row_stride = static_cast<uint32_t>(row_len);
+  a.col_stride = static_cast<uint32_t>(stride * h_f);
   a.M = static_cast<int>(c_out); a.Mp = Mp; a.K = static_cast<int>(K); a.Kp = Kp;
   a.n_gemm = static_cast<uint32_t>(n_gemm);
   a.c_in = static_cast<uint32_t>(c_in); a.h_out = static_cast<uint32_t>(h_out);

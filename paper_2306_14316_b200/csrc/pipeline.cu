@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "../../include/im2win_sm100.h"
@@ -57,6 +58,13 @@ struct Geometry {
 };
 
 size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+// FP32 chunks: windows gathered straight from NCHW (default) or via Ĩ (IM2WIN_FP32_PATH=windows),
+// the same rule as kernels.nchw_direct
+bool fp32_nchw_path() {
+  const char* e = getenv("IM2WIN_FP32_PATH");
+  return !(e && std::strcmp(e, "windows") == 0);
+}
 
 Geometry geometry(int64_t n_chunk, int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride,
                   int pad, int variant) {
@@ -245,6 +253,12 @@ static int host_conv(const float* host_in, const float* host_flt, float* host_ou
       if (!rc)
         rc = im2win_conv_fused(mid, d_flt, d_out[s], nk, c_in, h + 2 * pad, w + 2 * pad, c_out, h_f, w_f, stride,
                                variant, conv_ws, g.conv_ws, P.comp);
+    } else if (pad == 0 && (!plan || plan->micro_kernel) && fp32_nchw_path()) {
+      // the tiled kernel gathers the windows from the chunk's NCHW input (no Ĩ; same bits):
+      // input buffer s is free once the conv finishes
+      rc = im2win_conv_nchw_f32(d_in[s], d_flt, d_out[s], nk, c_in, h, w, c_out, h_f, w_f, stride, plan, variant,
+                                conv_ws, g.conv_ws, P.comp);
+      cudaEventRecord(P.xf_done[s], P.comp);
     } else {
       rc = im2win_transform_f32_padded(d_in[s], static_cast<float*>(mid), nk, c_in, h, w, h_f, w_f, stride, pad,
                                        P.comp);

@@ -69,6 +69,27 @@ def conv_windows_into(win: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, p
     _lib.check(rc)
 
 
+def conv_nchw_into(x: torch.Tensor, flt: torch.Tensor, out: torch.Tensor, params: ConvParams,
+                   plan: TilePlan | None = None, variant: str = "fp32-exact",
+                   ws: torch.Tensor | None = None) -> None:
+    """FP32 im2win convolution straight from the NCHW input (im2win_conv_nchw_f32): the tiled
+    kernel gathers each window element from x in the reference's k order, so no Ĩ is written
+    and the bits equal im2win_into + conv_windows_into."""
+    n_img, c_in, h_in, w_in = (int(d) for d in x.shape)
+    code = _variant_code(variant)
+    lib = _lib.load()
+    nbytes = lib.im2win_conv_workspace_bytes(c_in, params.c_out, params.h_f, params.w_f, code)
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    ws = _workspace(x.device, stream, nbytes) if ws is None else _check_ws(ws, nbytes)
+    cplan = to_c_plan(plan)
+    with torch.cuda.device(x.device):
+        rc = lib.im2win_conv_nchw_f32(x.data_ptr(), flt.data_ptr(), out.data_ptr(), n_img, c_in, h_in, w_in,
+                                      params.c_out, params.h_f, params.w_f, params.stride,
+                                      None if cplan is None else _byref(cplan), code, ws.data_ptr(), ws.numel(),
+                                      stream)
+    _lib.check(rc)
+
+
 def _byref(x):
     import ctypes
 
@@ -278,7 +299,11 @@ def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, 
                     variant: str = "fp32-exact", tc_path: str = "auto") -> Tensor4:
     """Window-order transform followed by the tiled kernel (optimized.py:237-241).
 
-    FP32 variants use the reference window layout Ĩ.  Tensor-core variants pick
+    FP32 variants: the tiled kernel gathers every im2win window element straight from the
+    NCHW input in the reference's k order (Ĩ[i,c,oh,(ow*s+fw)*Hf+fh] = X[i,c,oh*s+fh,ow*s+fw],
+    layouts.py:73-83), so Ĩ is never written and the bits equal `im2win` followed by
+    `compute_from_windows_opt`; with zero padding (or the micro_kernel=False ablation plan) the
+    transform to Ĩ runs first, in image chunks above the window budget.  Tensor-core variants pick
     (tc_path="auto"): "direct" — for few-channel inputs (C <= 16) producer warps
     build each pixel's im2win window in shared memory from the NCHW input;
     "fused" — TMA builds window tiles from a channels-last copy
@@ -326,7 +351,22 @@ def conv_im2win_opt(inp, flt, params: ConvParams, plan: TilePlan | None = None, 
         fd = f.data if f.device == i.device else f.data.to(i.device)
         conv_cl_into(win_cl, fd, out, params, variant)
         return Tensor4(out)
+    if variant in ("fp32-exact", "fp32-fma") and nchw_direct(params, plan):
+        fd = f.data if f.device == i.device else f.data.to(i.device)
+        out = torch.empty((i.dims[0], params.c_out, h_out, w_out), dtype=DTYPE, device=i.device)
+        conv_nchw_into(i.data, fd, out, params, plan, variant)
+        return Tensor4(out)
     return _fp32_chunked(i, f, params, plan, variant, h_out, w_out)
+
+
+def nchw_direct(params: ConvParams, plan: TilePlan | None = None) -> bool:
+    """Whether the FP32 conv_im2win_opt gathers its windows straight from the NCHW input
+    (im2win_conv_nchw_f32, no Ĩ written; the default) rather than transforming to Ĩ first.
+    Same bits either way.  Zero padding and the TilePlan(micro_kernel=False) ablation keep the
+    Ĩ path; IM2WIN_FP32_PATH=windows forces it (A/B)."""
+    if params.pad or (plan is not None and not plan.micro_kernel):
+        return False
+    return os.environ.get("IM2WIN_FP32_PATH", "nchw") != "windows"
 
 
 def window_budget_bytes() -> int:
@@ -577,6 +617,9 @@ class CapturedConv:
                 def body():
                     nhwc_into(self.input, self._mid, pad)
                     conv_fused_into(self._mid, self.filter, self.out, params, variant, self._ws)
+        elif nchw_direct(params, plan):
+            def body():
+                conv_nchw_into(self.input, self.filter, self.out, params, plan, variant, self._ws)
         else:
             from .layouts import effective_width, im2win_into
 

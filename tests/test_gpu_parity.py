@@ -884,3 +884,65 @@ def test_fp32_window_budget_chunks_bitwise(variant, monkeypatch, layer_goldens):
         monkeypatch.setenv("IM2WIN_WINDOW_BUDGET", "1")
         out = pkg.conv_im2win_opt(inp, flt, cfg.params).numpy()
         assert orc.checksum(out) == g["out_sha"]
+
+
+def test_nchw_direct_all_tiles_and_toggles_bitwise(small_cases):
+    """The FP32 kernels gathering windows straight from NCHW (im2win_conv_nchw_f32, the default
+    of conv_im2win_opt) give the reference's bits for every compiled CTA tile and toggle, on Fig. 1,
+    the special-values case, the 1x1 identity and the random geometries."""
+    from paper_2306_14316_b200.kernels import conv_nchw_into
+
+    names = ["fig1", "special", "identity1x1"] + [f"rand{i:03d}" for i in range(0, 200, 5)]
+    for name in names:
+        c = small_cases[name]
+        params = _params(c)
+        inp = torch.from_numpy(c["inp"]).to(DEV)
+        flt = torch.from_numpy(c["flt"]).to(DEV)
+        plans = [None]
+        for (bm, bn) in pkg.plan.SIMT_TILES:
+            for vec in (True, False):
+                for pf in (True, False):
+                    plans.append(pkg.TilePlan(bm, bn, 8, 8, 8, vectorized_load=vec, prefetch_double_buffer=pf))
+        plans += [pkg.TilePlan(bm, bn, 8, 4, 4) for (bm, bn) in pkg.plan.SIMT_TILES_MT4]
+        for plan in plans:
+            out = torch.full(c["out"].shape, float("nan"), device=DEV)
+            conv_nchw_into(inp, flt, out, params, plan)
+            assert bits_equal_nan_as_class(out.cpu().numpy(), c["out"]), (name, plan)
+
+
+@pytest.mark.parametrize("variant", ["fp32-exact", "fp32-fma"])
+def test_nchw_direct_equals_window_path_all_layers(variant, monkeypatch, layer_goldens):
+    """conv_im2win_opt (NCHW-direct) == im2win + compute_from_windows_opt bit for bit on all 12
+    layers (the golden checksums for fp32-exact), and on the small-K persistent kernel's shapes."""
+    for name in BENCHMARKS:
+        g = layer_goldens[name]
+        cfg = replace(BENCHMARKS[name], batch=g["batch"], seed=g["seed"])
+        inp, flt = make_inputs(cfg)
+        direct = pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant).numpy()
+        windows = pkg.compute_from_windows_opt(pkg.im2win(inp, cfg.params), flt, cfg.params,
+                                               variant=variant).numpy()
+        assert bits_equal(direct, windows), name
+        if variant == "fp32-exact":
+            assert orc.checksum(direct) == g["out_sha"], name
+    monkeypatch.setenv("IM2WIN_FP32_PATH", "windows")
+    g = layer_goldens["conv9"]
+    cfg = replace(BENCHMARKS["conv9"], batch=g["batch"], seed=g["seed"])
+    inp, flt = make_inputs(cfg)
+    assert bits_equal(pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant).numpy(),
+                      pkg.compute_from_windows_opt(pkg.im2win(inp, cfg.params), flt, cfg.params,
+                                                   variant=variant).numpy())
+
+
+def test_nchw_direct_large_batch_sampled_images():
+    """NCHW-direct FP32-exact at N=128 (conv4, conv7 small-K, conv12 4x4 tiles, conv1 96-wide
+    tiles and tail split): sampled images bitwise equal to the oracle."""
+    for name in ("conv4", "conv7", "conv12", "conv1"):
+        cfg = replace(BENCHMARKS[name], batch=128)
+        g = torch.Generator(device=DEV).manual_seed(77)
+        x = torch.randn((128, cfg.c_in, cfg.h_in, cfg.w_in), device=DEV, generator=g)
+        f = torch.randn((cfg.c_out, cfg.c_in, cfg.h_f, cfg.w_f), device=DEV, generator=g)
+        out = pkg.conv_im2win_opt(x, f, cfg.params)
+        fn = f.cpu().numpy()
+        for i in (0, 77, 127):
+            ref = orc.conv_direct(x[i:i + 1].cpu().numpy(), fn, cfg.stride)
+            assert bits_equal(out.data[i:i + 1].cpu().numpy(), ref), (name, i)
