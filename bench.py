@@ -130,27 +130,30 @@ def pcie_probe(dev, stream, nbytes: int = 256 << 20) -> dict:
             "d2h_gbs": timed(lambda: hd.copy_(db, non_blocking=True)), "bidir_each_gbs": timed(both)}
 
 
-def load_traffic(names, batch: int, variant: str):
-    """DRAM traffic of the step's kernels from the committed ncu --set full capture.
+def load_traffic(names, batch: int, variant: str, path: str = "windows"):
+    """DRAM traffic of the step's conv kernels from a committed ncu capture.
 
-    profiles/r01_traffic_n128.json is written by tools/ncu_traffic.py from one
-    `ncu --set full` capture per layer (dram__bytes_read.sum + dram__bytes_write.sum).
-    Returns None when it does not cover this workload.
+    path "windows" (conv over Ĩ): profiles/r01_traffic_n128.json, tools/ncu_traffic.py (one
+    `ncu --set full` capture per layer); path "nchw" (windows gathered from NCHW):
+    profiles/r02_traffic_nchw_n128.json, tools/ncu_traffic_nchw.py.  dram__bytes_read.sum +
+    dram__bytes_write.sum per conv call.  Returns None when no capture covers this workload.
     """
-    for p in sorted((ROOT / "profiles").glob("r*_traffic_n128.json"), reverse=True):
+    for p in sorted((ROOT / "profiles").glob("r*_traffic*_n128.json"), reverse=True):
         d = json.loads(p.read_text())
-        if d.get("batch") != batch or d.get("variant") != variant or not all(n in d["layers"] for n in names):
+        if (d.get("batch") != batch or d.get("variant") != variant or d.get("path", "windows") != path
+                or not all(n in d["layers"] for n in names)):
             continue
         conv = [d["layers"][n]["conv_dram_bytes"] for n in names]
-        xf = [d["layers"][n]["transform_dram_bytes"] for n in names]
         alg = [d["layers"][n]["conv_algorithmic_bytes"] for n in names]
-        return {"source": str(p.relative_to(ROOT)), "capture": d.get("capture"),
-                "conv_bytes_per_launch": sum(conv) / len(conv),
-                "per_launch_note": "per layer conv call (mean over the 12 layers); a tail-split layer's two "
-                                   "kernel launches count as one call",
-                "conv_algorithmic_bytes_per_launch": sum(alg) / len(alg),
-                "transform_bytes_per_launch": sum(xf) / len(xf),
-                "per_layer": {n: d["layers"][n] for n in names}}
+        out = {"source": str(p.relative_to(ROOT)), "capture": d.get("capture"),
+               "conv_bytes_per_launch": sum(conv) / len(conv),
+               "per_launch_note": "per layer conv call (mean over the 12 layers); a tail-split layer's two "
+                                  "kernel launches count as one call",
+               "conv_algorithmic_bytes_per_launch": sum(alg) / len(alg),
+               "per_layer": {n: d["layers"][n] for n in names}}
+        if all("transform_dram_bytes" in d["layers"][n] for n in names):
+            out["transform_bytes_per_launch"] = sum(d["layers"][n]["transform_dram_bytes"] for n in names) / len(names)
+        return out
     return None
 
 
@@ -492,6 +495,48 @@ def tc_layer(D, cfg_global, variant: str, reps: int = 5) -> dict:
             "per_rank_batch": cfg.batch}
 
 
+def windows_path_step(layers, variant: str, dev, stream, peaks, fp, D, reps: int = 5) -> dict:
+    """The reference's two-call form -- im2win transform, then the tiled conv over Ĩ
+    (layouts.py:86-95 + optimized.py:217-234) -- timed per layer after the headline region:
+    the transform's HBM GB/s against the roofline, and the step this form would give."""
+    import torch
+
+    from paper_2306_14316_b200.kernels import conv_windows_into
+    from paper_2306_14316_b200.layouts import im2win_into
+
+    rows, tot_f, tot_s = {}, 0.0, 0.0
+    for L in layers:
+        cfg = L["cfg"]
+        h_out, _ = cfg.out_dims
+        mid = torch.empty((cfg.batch, cfg.c_in, h_out, cfg.h_f * cfg.w_eff), device=dev)
+        tr = lambda: im2win_into(L["x"], mid, cfg.params)  # noqa: E731
+        cv = lambda: conv_windows_into(mid, L["f"], L["out"], cfg.params, cfg.w_eff, None, variant)  # noqa: E731
+        tr()
+        cv()
+        torch.cuda.synchronize(dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * reps)]
+        for r in range(reps):
+            ev[3 * r].record(stream)
+            tr()
+            ev[3 * r + 1].record(stream)
+            cv()
+            ev[3 * r + 2].record(stream)
+        torch.cuda.synchronize(dev)
+        t_tr = D.max(statistics.fmean(ev[3 * r].elapsed_time(ev[3 * r + 1]) for r in range(reps)))
+        t_cv = D.max(statistics.fmean(ev[3 * r + 1].elapsed_time(ev[3 * r + 2]) for r in range(reps)))
+        gbs = cfg.transform_bytes() / (t_tr * 1e-3) / 1e9
+        rows[L["name"]] = {"transform_ms": t_tr, "transform_gbs": gbs, "transform_frac_of_hbm": gbs / peaks["hbm_gbs"],
+                           "conv_ms": t_cv, "tflops": cfg.flops / ((t_tr + t_cv) * 1e-3) / 1e12,
+                           "tflops_conv_only": cfg.flops / (t_cv * 1e-3) / 1e12}
+        tot_f += cfg.flops
+        tot_s += (t_tr + t_cv) * 1e-3
+        del mid
+    torch.cuda.empty_cache()
+    return {"note": "im2win transform (TMA bulk copies) + conv over the materialised Ĩ, per layer, CUDA events, "
+                    f"mean of {reps} after a warm-up, max over ranks; same bits as the headline path",
+            "tflops_per_gpu": tot_f / tot_s / 1e12, "layers": rows}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -503,6 +548,8 @@ def main() -> None:
     ap.add_argument("--layers", default="all")
     ap.add_argument("--no-baselines", action="store_true", help="skip cuDNN / im2col+cuBLAS / CPU legs")
     ap.add_argument("--no-tc", action="store_true", help="skip the TF32/BF16 config-4/5 legs")
+    ap.add_argument("--windows-path", action="store_true",
+                    help="headline FP32 step as transform + conv over Ĩ instead of the production NCHW-direct call")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--detail", default="gpurun_out/bench_detail.json", help="sidecar file with every table")
     args = ap.parse_args()
@@ -521,8 +568,10 @@ def main() -> None:
         conv_direct_into,
         conv_fused_into,
         conv_fused_nchw_into,
+        conv_nchw_into,
         conv_windows_into,
         direct_preferred,
+        nchw_direct,
         nhwc_into,
         nhwc_pitch,
     )
@@ -549,7 +598,13 @@ def main() -> None:
         L["x"] = torch.randn((cfg.batch, cfg.c_in, cfg.h_in, cfg.w_in), device=dev, generator=gen)
         L["f"] = torch.randn((cfg.c_out, cfg.c_in, cfg.h_f, cfg.w_f), device=dev, generator=gen)
         L["out"] = torch.empty((cfg.batch, cfg.c_out, h_out, w_out), device=dev)
-        if not tc_step:
+        if not tc_step and nchw_direct(cfg.params) and not args.windows_path:
+            # production conv_im2win_opt: the tiled kernel gathers the im2win windows straight from
+            # NCHW (im2win_conv_nchw_f32; no Ĩ pass, same bits); the transform + conv over Ĩ (the
+            # compute_from_windows_opt seam) is timed after the headline region (detail.windows_path)
+            L["tr"] = lambda: None
+            L["cv"] = (lambda L=L: conv_nchw_into(L["x"], L["f"], L["out"], L["cfg"].params, None, args.variant))
+        elif not tc_step:
             L["mid"] = torch.empty((cfg.batch, cfg.c_in, h_out, cfg.h_f * cfg.w_eff), device=dev)
             L["tr"] = (lambda L=L: im2win_into(L["x"], L["mid"], L["cfg"].params))
             L["cv"] = (lambda L=L: conv_windows_into(L["mid"], L["f"], L["out"], L["cfg"].params, L["cfg"].w_eff,
@@ -632,15 +687,26 @@ def main() -> None:
         rec = {"transform_ms": t_tr, "conv_ms": t_cv, "tflops": cfg.flops / ((t_tr + t_cv) * 1e-3) / 1e12,
                "tflops_conv_only": cfg.flops / (t_cv * 1e-3) / 1e12, "kernel": kernel_of[L["name"]]}
         if not tc_step:
-            rec["transform_gbs"] = cfg.transform_bytes() / (t_tr * 1e-3) / 1e9
             pk = fp["exact"] if args.variant == "fp32-exact" else fp["ffma"]
-            rec["roofline"] = {"bound": "fp32-simt", "peak_tflops": pk, "frac": rec["tflops_conv_only"] / pk,
-                               "transform_frac_of_hbm": rec["transform_gbs"] / peaks["hbm_gbs"]}
+            rec["roofline"] = {"bound": "fp32-simt", "peak_tflops": pk, "frac": rec["tflops_conv_only"] / pk}
+            if "mid" in L:
+                rec["transform_gbs"] = cfg.transform_bytes() / (t_tr * 1e-3) / 1e9
+                rec["roofline"]["transform_frac_of_hbm"] = rec["transform_gbs"] / peaks["hbm_gbs"]
+            else:
+                rec["path"] = "windows gathered from NCHW (im2win_conv_nchw_f32), no transform pass"
         per_layer[L["name"]] = rec
+
+    windows_path = None
+    if not tc_step and not any("mid" in L for L in layers):
+        windows_path = windows_path_step(layers, args.variant, dev, stream, peaks, fp, D)
 
     detail = {"metric": METRIC, "n_gpus": world, "devices_distinct": D.devices_distinct, "backend": D.backend,
               "headline_step": {"variant": args.variant, "per_gpu_batch": args.batch, "value_tflops": value,
-                                "ms_per_step": ms_per_step, "layers": per_layer},
+                                "ms_per_step": ms_per_step, "layers": per_layer,
+                                "path": "conv_im2win_opt production path" + (
+                                    " (FP32: im2win windows gathered straight from NCHW, no Ĩ pass)"
+                                    if windows_path is not None else "")},
+              "windows_path": windows_path,
               "peaks": {"fp32_exact_tflops": fp["exact"], "fp32_ffma_tflops": fp["ffma"],
                         "hbm_gbs": peaks["hbm_gbs"], "bf16_tflops_file": peaks.get("bf16_tflops"),
                         "source": peaks["source"] + "; fp32 probes measured in this run"}}
@@ -746,7 +812,8 @@ def main() -> None:
             detail["cpu_baseline"] = cpu_baseline
 
     # ---- the compact driver line ----
-    traffic = load_traffic(names, args.batch, args.variant) if not tc_step else None
+    fp32_nchw = not tc_step and not any("mid" in L for L in layers)
+    traffic = load_traffic(names, args.batch, args.variant, "nchw" if fp32_nchw else "windows") if not tc_step else None
     if tc_step:
         pk = tpk[args.variant]
         roof = {"bound": "tensor", "kernel": "tcgen05 conv (per-layer kernels in detail)",
@@ -755,7 +822,8 @@ def main() -> None:
     else:
         pk = fp["exact"] if args.variant == "fp32-exact" else fp["ffma"]
         roof = {"bound": "fp32-simt", "kernel": "conv_simt_kernel " + ("FMUL+FADD" if args.variant == "fp32-exact"
-                                                                        else "FFMA"),
+                                                                        else "FFMA")
+                + (", windows gathered from NCHW" if fp32_nchw else ""),
                 "achieved": flops_step / (conv_ms_total * 1e-3) / 1e12, "peak": pk, "unit": "TFLOP/s",
                 "traffic": traffic and traffic["conv_bytes_per_launch"]}
     roof["frac"] = roof["achieved"] / roof["peak"]
@@ -777,7 +845,9 @@ def main() -> None:
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": {"fp32-exact": "f32", "fp32-fma": "f32", "tf32": "tf32", "bf16": "bf16"}[
             args.variant], "data": "synthetic N(0,1), torch.randn on device (seeded)",
-        "config": {"workload": f"paper 12 conv layers, im2win transform + {args.variant} conv, N={args.batch}/GPU",
+        "config": {"workload": (f"paper 12 conv layers, conv_im2win_opt {args.variant} (im2win windows gathered from "
+                                f"NCHW, no Ĩ pass), N={args.batch}/GPU" if fp32_nchw else
+                                f"paper 12 conv layers, im2win transform + {args.variant} conv, N={args.batch}/GPU"),
                    "global_batch": args.batch * world, "parallelism": f"batch-shard x{world}, no data-path collective",
                    "l2": "no flush: ~15 GB working set per step >> 126 MB L2"},
         "roofline": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in roof.items()},

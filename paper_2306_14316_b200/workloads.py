@@ -80,6 +80,11 @@ class BenchConfig:
         """Algorithmic HBM bytes of the convolution: read Ĩ and F once, write O once."""
         return operand_bytes * (self.elems("im2win") + self.filter_elems) + BYTES_PER_ELEM * self.out_elems
 
+    def conv_nchw_bytes(self) -> int:
+        """Algorithmic HBM bytes of the convolution that gathers its windows straight from the
+        input (no Ĩ): read X and F once, write O once."""
+        return BYTES_PER_ELEM * (self.elems("raw") + self.filter_elems + self.out_elems)
+
 
 def _cfg(name, c_in, h_in, w_in, c_out, h_f, w_f, stride) -> BenchConfig:
     return BenchConfig(name=name, c_in=c_in, h_in=h_in, w_in=w_in, c_out=c_out, h_f=h_f,
