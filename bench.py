@@ -397,11 +397,11 @@ def roofline_row(flops: float, nbytes: float, seconds: float, peak_tf: float, hb
 
 def _feed_chosen(cfg, variant: str) -> bool:
     """Mirror of the library's feed rule (conv_tc_fused.cu): the channels-last copy is produced
-    inside the conv kernel when output/input elements <= 0.5 and N <= 512, or when IM2WIN_FEED=2."""
+    inside the conv kernel when output/input elements <= 0.5 and N <= 256, or when IM2WIN_FEED=2."""
     mode = os.environ.get("IM2WIN_FEED", "1")
     h_out, w_out = cfg.out_dims
     r = cfg.c_out * h_out * w_out / (cfg.c_in * cfg.h_in * cfg.w_in)
-    return mode == "2" or (mode == "1" and r <= 0.5 and cfg.batch <= 512)
+    return mode == "2" or (mode == "1" and r <= 0.5 and cfg.batch <= 256)
 
 
 def tc_layer(D, cfg_global, variant: str, reps: int = 5) -> dict:

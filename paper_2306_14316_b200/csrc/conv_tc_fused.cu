@@ -633,18 +633,18 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
   // (counters at the end of the workspace, see im2win_tc_feed_counters)
   NhwcFeed feed{};
   if (feed_src) {
-    // In-kernel feed or a copy kernel first.  Measured (tools/feed_ab.py): the feed warps and the
-    // conv share the memory system, so overlap pays only where the conv's own traffic is light
-    // next to the input -- output/input elements r = (Co*Ho*Wo)/(C*H*W) <= 0.5 (strided layers:
-    // conv4 BF16 1.22 -> 1.02 ms, TF32 2.15 -> 1.81-1.89 ms at N=128; 4.80 -> 4.06 and
-    // 8.43 -> 7.34 ms at N=512) -- and not at N=2048 (conv4 BF16 19.0 vs 20.0 ms, TF32 33.1 vs
-    // 32.4-33.5 at any lookahead); at r ~ 0.9 (conv9/10) it ties or loses, at r >= 1.4 (conv5/6/8)
-    // it loses up to 18%.  IM2WIN_FEED: 0 never, 1 auto (r <= 0.5 and N <= 512), 2 always.
+    // In-kernel feed or a copy kernel first.  Measured (tools/feed_ab.py): the feed warps share the
+    // SM's L1/shared-memory datapath and HBM with the conv, so overlap pays only where the conv's
+    // own traffic is light next to the input -- output/input elements r = (Co*Ho*Wo)/(C*H*W) <= 0.5
+    // (strided layers: conv4 N=128 BF16 1.15 -> 1.02 ms, TF32 1.98 -> 1.82 ms) -- and only at small
+    // batches (conv4 N=512: BF16 4.48 -> 4.20 but TF32 7.81 -> 7.90; N=2048 slower for both); at
+    // r ~ 0.9 (conv9/10) it ties or loses, at r >= 1.4 (conv5/6/8) it loses up to 18%.
+    // IM2WIN_FEED: 0 never, 1 auto (r <= 0.5 and N <= 256), 2 always.
     const char* fe = getenv("IM2WIN_FEED");
     const int mode = fe ? atoi(fe) : 1;
     const int64_t h_o = (h - h_f) / stride + 1, w_o = (w - w_f) / stride + 1;
     const double r = static_cast<double>(c_out * h_o * w_o) / static_cast<double>(c_in * h * w);
-    if (mode == 0 || (mode == 1 && (r > 0.5 || n > 512))) {
+    if (mode == 0 || (mode == 1 && (r > 0.5 || n > 256))) {
       const int rc = im2win_launch_nchw_to_nhwc(feed_src, const_cast<void*>(x_cl), n, c_in, h, w, bf16, 0, stream, err);
       if (rc) return rc;
       feed_src = nullptr;

@@ -74,7 +74,9 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
   const uint32_t a_box_bytes = loaded_rows * kRowBytes;
   const uint32_t s = a.stride;
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
-  const uint32_t unit = blockIdx.x / kCtas, units = gridDim.x / kCtas;  // CTA or CTA pair
+  // work items walk per CTA (or per CTA pair): t = blockIdx.x [/ 2] + k * gridDim.x [/ 2], written
+  // out at each loop -- a hoisted unit/units pair made ptxas move the MMA warp's descriptor math
+  // from uniform to regular registers (R2UR per MMA; conv4 10% slower)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -118,14 +120,14 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       uint32_t conf_lo = 1, conf_hi = 0;
-      for (uint32_t t = unit; t < total; t += units) {
+      for (uint32_t t = PAIR ? blockIdx.x / 2 : blockIdx.x; t < total; t += PAIR ? gridDim.x / 2 : gridDim.x) {
         const uint32_t co_blk = t % a.co_tiles;
         const uint32_t pair = t / a.co_tiles;
         uint32_t ow0[MT], oh0[MT], n0[MT];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           // past the last pixel tile: coordinates past the tensor (TMA zero-fills), D not stored
-          uint32_t pt = (pair * kCtas + rank) * MT + mt;
+          uint32_t pt = (PAIR ? pair * 2 + rank : pair) * MT + mt;
           ow0[mt] = (pt % a.ow_tiles) * a.box_w;
           pt /= a.ow_tiles;
           oh0[mt] = (pt % a.oh_tiles) * a.rows;
@@ -180,9 +182,50 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if constexpr (!PAIR) {
+      // (the single-lane issue loop exactly as before the pair variant: ptxas keeps its descriptor
+      // arithmetic in uniform registers; variants of it measured 10% slower on conv4)
+      if (lane == 0) {
+        uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+        for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+          mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t tmem_d = tmem_base + acc * (MT * N);
+          for (uint32_t ki = 0; ki < a.k_iters; ++ki) {
+            const uint32_t r = (ki / a.c_slabs) % s;
+            const uint32_t nq = (a.w_f - r + s - 1) / s;
+            mbar_wait(&full_bar[stage], phase);
+            tc_fence_after();
+            const uint32_t abase = smem_u32(smem + stage * kStageBytes);
+            const uint32_t bbase = abase + kABytes;
+#pragma unroll
+            for (int q = 0; q < TAPS; ++q) {
+              if (q < static_cast<int>(nq)) {
+#pragma unroll
+                for (int kk = 0; kk < kBK / kUK; ++kk) {
+                  const uint64_t bd = smem_desc_sw128(bbase + q * kBTap + kk * 32);
+#pragma unroll
+                  for (int mt = 0; mt < MT; ++mt)
+#ifdef IM2WIN_PHASE_NOSHIFT  // exploration builds only: wrong results, times an unshifted A read
+                    mma<BF16>(tmem_d + mt * N, smem_desc_sw128(abase + mt * kATile + kk * 32), bd, kIdesc,
+                              (ki | q | kk) != 0);
+#else
+                    mma<BF16>(tmem_d + mt * N, smem_desc_sw128(abase + mt * kATile + q * kRowBytes + kk * 32), bd,
+                              kIdesc, (ki | q | kk) != 0);
+#endif
+                }
+              }
+            }
+            mma_commit(&empty_bar[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          mma_commit(&tfull_bar[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+      }
+    } else if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (uint32_t t = unit; t < total; t += units) {
+      for (uint32_t t = PAIR ? blockIdx.x / 2 : blockIdx.x; t < total; t += PAIR ? gridDim.x / 2 : gridDim.x) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * (MT * N);
@@ -200,24 +243,16 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
               for (int kk = 0; kk < kBK / kUK; ++kk) {
                 const uint64_t bd = smem_desc_sw128(bbase + q * kBTap + kk * 32);
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt) {
-#ifdef IM2WIN_PHASE_NOSHIFT  // exploration builds only: wrong results, times an unshifted A read
-                  const uint64_t ad = smem_desc_sw128(abase + mt * kATile + kk * 32);
-#else
-                  const uint64_t ad = smem_desc_sw128(abase + mt * kATile + q * kRowBytes + kk * 32);
-#endif
-                  if constexpr (PAIR) mma_pair<BF16>(tmem_d + mt * N, ad, bd, kIdesc, (ki | q | kk) != 0);
-                  else mma<BF16>(tmem_d + mt * N, ad, bd, kIdesc, (ki | q | kk) != 0);
-                }
+                for (int mt = 0; mt < MT; ++mt)
+                  mma_pair<BF16>(tmem_d + mt * N, smem_desc_sw128(abase + mt * kATile + q * kRowBytes + kk * 32), bd,
+                                 kIdesc, (ki | q | kk) != 0);
               }
             }
           }
-          if constexpr (PAIR) mma_commit_pair(&empty_bar[stage]);
-          else mma_commit(&empty_bar[stage]);
+          mma_commit_pair(&empty_bar[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        if constexpr (PAIR) mma_commit_pair(&tfull_bar[acc]);
-        else mma_commit(&tfull_bar[acc]);
+        mma_commit_pair(&tfull_bar[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -233,18 +268,19 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
     const uint32_t r_n = rr / per_img, r_rem = rr % per_img;
     const uint32_t r_h = r_rem / a.pitch, r_w = r_rem % a.pitch;
     uint32_t acc = 0, acc_phase = 0;
-    for (uint32_t t = unit; t < total; t += units) {
+    for (uint32_t t = PAIR ? blockIdx.x / 2 : blockIdx.x; t < total; t += PAIR ? gridDim.x / 2 : gridDim.x) {
       const uint32_t co_blk = t % a.co_tiles;
       const uint32_t pair = t / a.co_tiles;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+#ifndef IM2WIN_PHASE_EPI_TILEMAJOR
       // the MT tiles' pieces of each channel plane are stored back to back (consecutive output
       // rows of a plane: longer DRAM write runs, tools/probes/nchw_store_probe.cu)
       int64_t obase[MT];
       bool valid[MT];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
-        uint32_t pt = (pair * kCtas + rank) * MT + mt;
+        uint32_t pt = (PAIR ? pair * 2 + rank : pair) * MT + mt;
         const bool tile_ok = pt < a.p_tiles;
         const uint32_t ow = (pt % a.ow_tiles) * a.box_w + r_w;
         pt /= a.ow_tiles;
@@ -274,6 +310,34 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
         if (valid[0] && v[0][0] == 0x7fffffffu) a.out[obase[0]] = 0.f;
 #endif
       }
+#else
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        uint32_t pt = (PAIR ? pair * 2 + rank : pair) * MT + mt;
+        const bool tile_ok = pt < a.p_tiles;
+        const uint32_t ow = (pt % a.ow_tiles) * a.box_w + r_w;
+        pt /= a.ow_tiles;
+        const uint32_t oh = (pt % a.oh_tiles) * a.rows + r_h;
+        const uint32_t img = (pt / a.oh_tiles) * a.box_n + r_n;
+        const bool valid =
+            tile_ok && rr < loaded_rows && r_w < a.box_w && ow < a.w_out && oh < a.h_out && img < a.n_img;
+        const int64_t obase =
+            valid ? static_cast<int64_t>(img) * a.co * a.hw + static_cast<int64_t>(oh) * a.w_out + ow : 0;
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * (MT * N) + mt * N;
+#pragma unroll
+        for (int jj = 0; jj < N / 2; jj += 16) {
+          const int j0 = j_lo + jj;
+          uint32_t v[16];
+          tmem_ld16(taddr + j0, v);
+          const uint32_t m0 = co_blk * N + j0;
+          if (valid) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (m0 + q < a.co) st_out(a.out + obase + static_cast<int64_t>(m0 + q) * a.hw, __uint_as_float(v[q]));
+          }
+        }
+      }
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {

@@ -89,6 +89,40 @@ IM2WIN_DEVICE void mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t
   }
 }
 
+// Warp-converged MMA issue: the whole warp runs the issue loop (descriptors and loop state stay
+// warp-uniform, so they live in uniform registers) and elect.sync picks the one issuing lane.
+// With the loop inside `if (lane == 0)` ptxas wraps every UTCHMMA in an elect loop and moves the
+// descriptors through R2UR (measured: phase kernel conv4 10% slower).
+template <bool BF16, bool PAIR = false>
+IM2WIN_DEVICE void mma_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+#define IM2WIN_MMA_WARP(GROUP, KIND)                                                                     \
+  asm volatile(                                                                                          \
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"             \
+      "@e tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),  \
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate))
+  if constexpr (PAIR && BF16) IM2WIN_MMA_WARP("2", "f16");
+  else if constexpr (PAIR) IM2WIN_MMA_WARP("2", "tf32");
+  else if constexpr (BF16) IM2WIN_MMA_WARP("1", "f16");
+  else IM2WIN_MMA_WARP("1", "tf32");
+#undef IM2WIN_MMA_WARP
+}
+template <bool PAIR = false>
+IM2WIN_DEVICE void mma_commit_warp(uint64_t* bar) {
+  if constexpr (PAIR) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n"
+        ::"r"(smem_u32(bar)), "h"(static_cast<uint16_t>(3))
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+            smem_u32(bar))
+        : "memory");
+  }
+}
+
 IM2WIN_DEVICE void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                : "memory");
@@ -211,7 +245,11 @@ IM2WIN_DEVICE void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
 // other, so the kernel is launched cooperatively (all CTAs co-resident, or no launch).
 // The ready counters are zeroed by the host before the launch (cudaMemsetAsync).
 constexpr int kFeedWarps = 8;
+#ifndef IM2WIN_TC_BOUND_THREADS
 constexpr int kTcThreadsFeed = kTcThreads + 32 * kFeedWarps;
+#else  // exploration builds: launch bounds of the non-feed kernel (the feed then cannot launch)
+constexpr int kTcThreadsFeed = IM2WIN_TC_BOUND_THREADS;
+#endif
 
 // A unit: G channels (one 32-byte run of Xcl per pixel) x 32*J pixels; each lane loads
 // G*J values (one coalesced 128-byte row per channel and j) before storing any.
