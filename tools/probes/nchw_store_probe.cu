@@ -191,6 +191,44 @@ __global__ void __launch_bounds__(256) pattern_grouped(float* out, int n, int co
   }
 }
 
+// Variant: the TC epilogue staged through shared memory -- 8 warps, warp w owning lane quarter
+// w % 4 (32 pixels) and channel half w / 4 of a `group`-tile run (both halves of an output row
+// for group 2); each warp writes its values into smem [co][group*box_w] (lane = pixel), one
+// barrier, then warp w writes channel rows c = w, w+8, ... as whole runs (lane = pixel,
+// consecutive 128-byte pieces of the same plane row back to back).
+__global__ void __launch_bounds__(256) pattern_staged(float* out, int n, int co, int ho, int wo, int box_w, int group) {
+  extern __shared__ float stg[];  // [co][group * box_w]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int quarter = warp % 4, half = warp / 4;
+  const int ow_tiles = (wo + box_w - 1) / box_w;
+  const long long tiles = (long long)n * ho * ow_tiles;
+  const int r = quarter * 32 + lane;
+  const int pitch = group * box_w;
+  const long long hw = (long long)ho * wo;
+  for (long long t0 = (long long)blockIdx.x * group; t0 < tiles; t0 += (long long)gridDim.x * group) {
+    // stage: like tcgen05.ld -> st.shared, per tile of the run
+    for (int g = 0; g < group && t0 + g < tiles; ++g) {
+      if (r < box_w) {
+        const int c0 = half * (co / 2);
+#pragma unroll 8
+        for (int c = 0; c < co / 2; ++c) stg[(c0 + c) * pitch + g * box_w + r] = (float)(c0 + c);
+      }
+    }
+    __syncthreads();
+    // write: the run's pixels are consecutive in each plane (group tiles = whole rows)
+    const int owt = t0 % ow_tiles;
+    const long long rest = t0 / ow_tiles;
+    const int oh = rest % ho;
+    const long long img = rest / ho;
+    const int run = min(pitch, wo - owt * box_w);
+    for (int c = warp; c < co; c += 8) {
+      float* base = out + (img * co + c) * hw + (long long)oh * wo + owt * box_w;
+      for (int px = lane; px < run; px += 32) base[px] = stg[c * pitch + px];
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void fill(float4* out, long long n4) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x)
     out[i] = make_float4(1.f, 2.f, 3.f, 4.f);
@@ -288,6 +326,16 @@ int main() {
     cudaEventRecord(e0); pattern_grouped<<<148, 256>>>(out, n, co, ho, wo, 111, g); cudaEventRecord(e1);
     cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
     printf("grouped box_w=111 group=%d: %.3f ms  %.2f TB/s\n", g, ms, elems * 4 / (ms * 1e-3) / 1e12);
+  }
+  for (int g : {1, 2}) {
+    float ms;
+    const size_t sm = (size_t)co * g * 111 * 4;
+    cudaFuncSetAttribute(pattern_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    pattern_staged<<<148, 256, sm>>>(out, n, co, ho, wo, 111, g);
+    cudaEventRecord(e0); pattern_staged<<<148, 256, sm>>>(out, n, co, ho, wo, 111, g); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+    printf("staged box_w=111 group=%d: %.3f ms  %.2f TB/s (%s)\n", g, ms, elems * 4 / (ms * 1e-3) / 1e12,
+           cudaGetErrorString(cudaGetLastError()));
   }
   fill<<<148 * 8, 256>>>((float4*)out, elems / 4);
   cudaEventRecord(e0);
