@@ -196,7 +196,9 @@ IM2WIN_DEVICE void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 #define IM2WIN_ST_MODE 1
 #endif
 IM2WIN_DEVICE void st_out(float* p, float v) {
-#if IM2WIN_ST_MODE == 1
+#if IM2WIN_ST_MODE == 9  // exploration: no output stores (wrong results; times the rest of the kernel)
+  if (__float_as_uint(v) == 0x7fffffffu) *p = v;
+#elif IM2WIN_ST_MODE == 1
   __stcs(p, v);
 #elif IM2WIN_ST_MODE == 2 || IM2WIN_ST_MODE == 3
   uint64_t pol;

@@ -229,6 +229,74 @@ __global__ void __launch_bounds__(256) pattern_staged(float* out, int n, int co,
   }
 }
 
+// Variant: 8 stager warps (the TC epilogue: lane = pixel values into smem [co][2*box_w], both
+// halves of an output row) and 8 writer warps that only copy staged rows out (channel rows as
+// whole runs, lane = pixel), double-buffered with mbarriers so the writers never wait on a
+// barrier the stagers hold.
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(unsigned long long* b, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(unsigned long long* b, unsigned ph) {
+  asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}" ::"r"(
+                   su32(b)), "r"(ph) : "memory");
+}
+__global__ void __launch_bounds__(512) pattern_writers(float* out, int n, int co, int ho, int wo, int box_w) {
+  extern __shared__ float stg[];  // [2][co][2 * box_w]
+  __shared__ unsigned long long full[2], empty[2];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int pitch = 2 * box_w;
+  const long long rows = (long long)n * ho;
+  const long long hw = (long long)ho * wo;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) { bar_init(&full[b], 8); bar_init(&empty[b], 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int it = 0;
+  if (warp < 8) {  // stagers
+    const int quarter = warp % 4, half = warp / 4;
+    for (long long row = blockIdx.x; row < rows; row += gridDim.x, ++it) {
+      const int b = it & 1;
+      if (it >= 2) bar_wait(&empty[b], ((it >> 1) - 1) & 1);
+      float* sb = stg + b * co * pitch;
+      for (int g = 0; g < 2; ++g) {
+        const int r = quarter * 32 + lane;
+        if (r < box_w) {
+          const int c0 = half * (co / 2);
+#pragma unroll 8
+          for (int c = 0; c < co / 2; ++c) sb[(c0 + c) * pitch + g * box_w + r] = (float)(c0 + c);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) bar_arrive(&full[b]);
+    }
+  } else {  // writers
+    const int ww = warp - 8;
+    for (long long row = blockIdx.x; row < rows; row += gridDim.x, ++it) {
+      const int b = it & 1;
+      bar_wait(&full[b], (it >> 1) & 1);
+      const float* sb = stg + b * co * pitch;
+      const int oh = row % ho;
+      const long long img = row / ho;
+      for (int c = ww; c < co; c += 8) {
+        float* base = out + (img * co + c) * hw + (long long)oh * wo;
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = (q * 32 + lane < wo) ? sb[c * pitch + q * 32 + lane] : 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q * 32 + lane < wo) base[q * 32 + lane] = v[q];
+      }
+      __syncwarp();
+      if (lane == 0) bar_arrive(&empty[b]);
+    }
+  }
+}
+
 __global__ void fill(float4* out, long long n4) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x)
     out[i] = make_float4(1.f, 2.f, 3.f, 4.f);
@@ -336,6 +404,16 @@ int main() {
     cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
     printf("staged box_w=111 group=%d: %.3f ms  %.2f TB/s (%s)\n", g, ms, elems * 4 / (ms * 1e-3) / 1e12,
            cudaGetErrorString(cudaGetLastError()));
+  }
+  {
+    float ms;
+    const size_t sm = 2ull * co * 2 * 111 * 4;
+    cudaFuncSetAttribute(pattern_writers, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    pattern_writers<<<148, 512, sm>>>(out, n, co, ho, wo, 111);
+    cudaEventRecord(e0); pattern_writers<<<148, 512, sm>>>(out, n, co, ho, wo, 111); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+    printf("writers (8 stagers + 8 row writers, double buffer): %.3f ms  %.2f TB/s (%s)\n", ms,
+           elems * 4 / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
   }
   fill<<<148 * 8, 256>>>((float4*)out, elems / 4);
   cudaEventRecord(e0);
