@@ -210,14 +210,19 @@ struct TileWalk {
 // RB: the whole packed filter (k_slabs tiles of N x 128 B) is loaded once per CTA and
 // stays resident; only window tiles stream through the ring (small filters: the
 // 3-channel input layers, where staging the filter per tile doubles the TMA rows).
-template <bool BF16, int N, int STAGES, bool RB = false>
+//
+// ROW = 64: 64-byte K rows (SW64) instead of 128 (SW128), for inputs whose window row Wf * C_pad
+// fits in 64 bytes (conv7: 3 taps x 8 bf16 channels = 48 B) -- half the TMA bytes and half the
+// MMAs of 128-byte rows, most of which are channel padding there.
+template <bool BF16, int N, int STAGES, bool RB = false, int ROW = 128>
 __global__ void __launch_bounds__(kTcThreadsFeed, 1)
     conv_tc_fused_kernel(const FusedArgs a, const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b, const NhwcFeed feed) {
-  constexpr uint32_t kABytes = kTileM * kRowBytes;
-  constexpr uint32_t kBBytes = RB ? 0 : N * kRowBytes;
+  constexpr uint32_t kRowB = ROW;
+  constexpr uint32_t kABytes = kTileM * kRowB;
+  constexpr uint32_t kBBytes = RB ? 0 : N * kRowB;
   constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  constexpr int kBK = BF16 ? 64 : 32;
+  constexpr int kBK = (BF16 ? 64 : 32) * ROW / 128;
   constexpr int kUK = BF16 ? 16 : 8;
   constexpr uint32_t kTmemCols = (2 * N <= 128) ? 128 : (2 * N <= 256 ? 256 : 512);
   constexpr uint32_t kIdesc = instr_desc<BF16, N>();
@@ -234,9 +239,9 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const uint32_t pix_per_tile = a.box_w * a.box_h * a.box_n;
-  const uint32_t a_box_bytes = pix_per_tile * kRowBytes;
+  const uint32_t a_box_bytes = pix_per_tile * kRowB;
   // RB: resident filter tiles first, then the A ring
-  const uint32_t rb_bytes = RB ? a.k_slabs * N * kRowBytes : 0;
+  const uint32_t rb_bytes = RB ? a.k_slabs * N * kRowB : 0;
   uint8_t* smem = smem_base + rb_bytes;
 
   if (threadIdx.x == 0) {
@@ -270,7 +275,7 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
       if constexpr (RB) {  // requires co_tiles == 1 (host-checked)
         mbar_arrive_expect_tx(&bres_bar, rb_bytes);
         for (uint32_t ks = 0; ks < a.k_slabs; ++ks)
-          tma_load_2d(smem_base + ks * N * kRowBytes, &tmap_b, &bres_bar, ks * kBK, 0);
+          tma_load_2d(smem_base + ks * N * kRowB, &tmap_b, &bres_bar, ks * kBK, 0);
       }
       uint32_t conf_lo = 1, conf_hi = 0;
       for (TileWalk w(a.group); w.t < total_tiles; w.next()) {
@@ -310,10 +315,10 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t abase = smem_u32(smem + stage * kStageBytes);
-          const uint32_t bbase = RB ? smem_u32(smem_base) + ks * N * kRowBytes : abase + kABytes;
+          const uint32_t bbase = RB ? smem_u32(smem_base) + ks * N * kRowB : abase + kABytes;
 #pragma unroll
           for (int kk = 0; kk < kBK / kUK; ++kk)
-            mma<BF16>(tmem_d, smem_desc_sw128(abase + kk * 32), smem_desc_sw128(bbase + kk * 32), kIdesc,
+            mma<BF16>(tmem_d, smem_desc_row<ROW>(abase + kk * 32), smem_desc_row<ROW>(bbase + kk * 32), kIdesc,
                       (ks | kk) != 0);
           mma_commit(&empty_bar[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -396,11 +401,12 @@ __global__ void pack_filter_fused_kernel(const float* __restrict__ flt, void* __
   }
 }
 
-template <bool BF16, int N, int STAGES, bool RB = false>
+template <bool BF16, int N, int STAGES, bool RB = false, int ROW = 128>
 static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64_t c_in, int64_t h, int64_t w,
                         int32_t h_f, int32_t w_f, int32_t stride, int64_t Kp, int64_t Mp, const NhwcFeed& feed,
                         cudaStream_t stream, const char** err) {
-  constexpr int kBK = BF16 ? 64 : 32;
+  constexpr int kBK = (BF16 ? 64 : 32) * ROW / 128;
+  constexpr CUtensorMapSwizzle kSwz = ROW == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
   auto enc = get_encode_fn();
   if (!enc) {
     *err = "conv_tc_fused: cuTensorMapEncodeTiled unavailable";
@@ -418,7 +424,7 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
     cuuint32_t box[5] = {static_cast<cuuint32_t>(kBK), 1, a.box_w, a.box_h, a.box_n};
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     CUresult r = enc(&map_a, dt, 5, const_cast<void*>(x_cl), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     kSwz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       *err = "conv_tc_fused: window tensor map rejected (cuTensorMapEncodeTiled)";
       return 2;
@@ -430,7 +436,7 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
     cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(N)};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(&map_b, dt, 2, const_cast<void*>(packed), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     kSwz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       *err = "conv_tc_fused: filter tensor map rejected (cuTensorMapEncodeTiled)";
       return 2;
@@ -445,9 +451,9 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
     const int g = g_env ? atoi(g_env) : (a.ow_tiles > 1 && a.co_tiles == 1 && tiles >= 4ull * 32 * 148 ? 4 : 1);
     a.group = static_cast<uint32_t>(g < 1 ? 1 : g);
   }
-  const size_t rb = RB ? static_cast<size_t>(a.k_slabs) * N * kRowBytes : 0;
-  const size_t smem = rb + static_cast<size_t>(STAGES) * (kTileM + (RB ? 0 : N)) * kRowBytes + 1024;
-  auto kern = conv_tc_fused_kernel<BF16, N, STAGES, RB>;
+  const size_t rb = RB ? static_cast<size_t>(a.k_slabs) * N * ROW : 0;
+  const size_t smem = rb + static_cast<size_t>(STAGES) * (kTileM + (RB ? 0 : N)) * ROW + 1024;
+  auto kern = conv_tc_fused_kernel<BF16, N, STAGES, RB, ROW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
@@ -458,6 +464,10 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t tiles = static_cast<uint64_t>(a.n_tiles) * a.oh_tiles * a.ow_tiles * a.co_tiles;
   const uint32_t grid = tiles < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(tiles) : static_cast<uint32_t>(sms);
+  if (ROW == 64)
+    im2win_note_kernel(BF16 ? "conv_tc_fused_kernel (generic TMA window boxes, filter resident, 64-byte rows, bf16)"
+                            : "conv_tc_fused_kernel (generic TMA window boxes, filter resident, 64-byte rows, tf32)");
+  else
   im2win_note_kernel(RB ? (BF16 ? "conv_tc_fused_kernel (generic TMA window boxes, filter resident, bf16)"
                               : "conv_tc_fused_kernel (generic TMA window boxes, filter resident, tf32)")
                      : (BF16 ? "conv_tc_fused_kernel (generic TMA window boxes, bf16)"
@@ -722,6 +732,13 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
   const int64_t Mp = (c_out + N - 1) / N * N;
   a.fh_slabs = static_cast<uint32_t>(Kfh / bk);
   a.k_slabs = a.fh_slabs * h_f;
+  // 64-byte K rows when a filter row's window (Wf * C_pad elements) fits in 64 bytes and the filter
+  // stays resident (conv7: BF16 0.656 -> 0.596 ms at N=128, same bits -- the box rows, not their
+  // bytes, bound this layer); IM2WIN_ROW64=0 keeps 128-byte rows
+  const int64_t esz = bf16 ? 2 : 4;
+  const char* r64e = getenv("IM2WIN_ROW64");
+  const bool row64 = !(r64e && atoi(r64e) == 0) && w_f * cp * esz <= 64 && Mp == N && N <= 128;
+  const int bk64 = bf16 ? 32 : 16;
   {
     // the phase kernel reuses each loaded A tile for every tap of a stride phase (any stride <= 2)
     const double util = static_cast<double>(a.box_w) * a.box_h * a.box_n / kTileM;
@@ -735,6 +752,33 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
     const int rc = im2win_try_conv_tc_shift(x_cl, flt, out, workspace, n, c_in, cp, h, w, c_out, h_f, w_f, stride,
                                             bf16, util, feed, stream, err);
     if (rc != 0) return rc > 0 ? 0 : -rc;
+  }
+  if (row64) {
+    // one 64-byte slab per filter row: repack with Kfh = 32 (bf16) / 16 (tf32) and launch
+    FusedArgs b = a;
+    b.fh_slabs = 1;
+    b.k_slabs = static_cast<uint32_t>(h_f);
+    const int64_t Kp64 = static_cast<int64_t>(bk64) * h_f;
+    if (bf16)
+      pack_filter_fused_kernel<true><<<256, 256, 0, stream>>>(flt, workspace, static_cast<int>(c_out),
+                                                              static_cast<int>(c_in), static_cast<int>(cp), h_f, w_f,
+                                                              static_cast<int>(Mp), bk64, static_cast<int>(Kp64));
+    else
+      pack_filter_fused_kernel<false><<<256, 256, 0, stream>>>(flt, workspace, static_cast<int>(c_out),
+                                                               static_cast<int>(c_in), static_cast<int>(cp), h_f, w_f,
+                                                               static_cast<int>(Mp), bk64, static_cast<int>(Kp64));
+#define IM2WIN_FU64(BF, NN) \
+  return launch_fused<BF, NN, 8, true, 64>(b, x_cl, workspace, cp, h, w, h_f, w_f, stride, Kp64, Mp, feed, stream, err)
+    if (bf16) {
+      if (N == 64) IM2WIN_FU64(true, 64);
+      if (N == 96) IM2WIN_FU64(true, 96);
+      IM2WIN_FU64(true, 128);
+    } else {
+      if (N == 64) IM2WIN_FU64(false, 64);
+      if (N == 96) IM2WIN_FU64(false, 96);
+      IM2WIN_FU64(false, 128);
+    }
+#undef IM2WIN_FU64
   }
   if (bf16)
     pack_filter_fused_kernel<true><<<256, 256, 0, stream>>>(flt, workspace, static_cast<int>(c_out),

@@ -66,6 +66,22 @@ IM2WIN_DEVICE uint64_t smem_desc_sw128(uint32_t addr) {
   return d;
 }
 
+// K-major, 64-byte swizzle (rows of 64 B): 8-row atoms of 512 B (SBO), layout type 4 (sm_100)
+IM2WIN_DEVICE uint64_t smem_desc_sw64(uint32_t addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>(512 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(4) << 61;
+  return d;
+}
+template <int ROW>
+IM2WIN_DEVICE uint64_t smem_desc_row(uint32_t addr) {
+  if constexpr (ROW == 64) return smem_desc_sw64(addr);
+  else return smem_desc_sw128(addr);
+}
+
 template <bool BF16, int N>
 __host__ __device__ constexpr uint32_t instr_desc() {
   // c_format F32 (bit 4), a/b format (bits 7-9 / 10-12: BF16=1, TF32=2), K-major A and B,

@@ -946,3 +946,32 @@ def test_nchw_direct_large_batch_sampled_images():
         for i in (0, 77, 127):
             ref = orc.conv_direct(x[i:i + 1].cpu().numpy(), fn, cfg.stride)
             assert bits_equal(out.data[i:i + 1].cpu().numpy(), ref), (name, i)
+
+
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_tc_fused_64byte_rows(variant, monkeypatch, layer_goldens):
+    """The fused kernel with 64-byte K rows (window rows Wf * C_pad that fit in 64 bytes: conv7 and
+    few-channel odd shapes) gives the same bits as 128-byte rows (the extra K of those is zero
+    padding) and stays within tolerance of the oracle."""
+    from paper_2306_14316_b200 import _lib
+
+    g = layer_goldens["conv7"]
+    cfg = replace(BENCHMARKS["conv7"], batch=g["batch"], seed=g["seed"])
+    cases = [(make_inputs(cfg), cfg.params)]
+    for (n, c, h, w, co, hf, wf, s) in [(3, 3, 17, 21, 64, 3, 3, 1), (2, 2, 12, 13, 96, 3, 3, 2),
+                                        (1, 4, 30, 31, 128, 2, 2, 1), (2, 1, 9, 10, 64, 3, 5, 1)]:
+        rng = np.random.default_rng(n * 100 + c)
+        cases.append(((rng.standard_normal((n, c, h, w), dtype=np.float32),
+                       rng.standard_normal((co, c, hf, wf), dtype=np.float32)), pkg.ConvParams(c, co, hf, wf, s)))
+    for (inp, flt), params in cases:
+        monkeypatch.setenv("IM2WIN_ROW64", "1")
+        r64 = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path="fused").numpy()
+        kern = _lib.last_kernel()
+        monkeypatch.setenv("IM2WIN_ROW64", "0")
+        r128 = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path="fused").numpy()
+        assert bits_equal(r64, r128), (params, kern)
+        assert pkg.normalized_max_diff(r64, orc.conv_direct(inp, flt, params.stride)) <= TC_TOL[variant], params
+    monkeypatch.setenv("IM2WIN_ROW64", "1")
+    inp, flt = cases[0][0]
+    pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant, tc_path="fused")
+    assert "64-byte rows" in _lib.last_kernel()
