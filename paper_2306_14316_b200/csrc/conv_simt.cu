@@ -49,6 +49,9 @@
 #ifndef IM2WIN_SIMT_INTERLEAVE
 #define IM2WIN_SIMT_INTERLEAVE 1
 #endif
+#ifndef IM2WIN_SIMT_KTAIL
+#define IM2WIN_SIMT_KTAIL 1  // padded last K slab computed over its real rows only
+#endif
 #ifndef IM2WIN_SIMT_SDELTA
 #define IM2WIN_SIMT_SDELTA 1
 #endif
@@ -114,7 +117,9 @@ IM2WIN_DEVICE float mac(float acc, float a, float b) {
 // (its global-load latency otherwise sits on the gather's critical path).
 // The gather of slab kt+STAGES-1 is issued in BK/4 parts interleaved with the
 // compute of slab kt, so the 4-byte async copies do not arrive as one burst.
-template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC, int MT, bool SD>
+// PADK: K is not a multiple of BK, so the last slab holds padded k (delta -1, zero fill).
+// Without padded k every gathered element is a plain copy: no per-element predicate.
+template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC, int MT, bool SD, bool PADK = true>
 __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? ((BM / MT) * (BN / MT) <= 192 ? IM2WIN_SIMT_MINB192 : 2) : ((BM / MT) * (BN / MT) >= 512 ? 1 : 3))
     conv_simt_kernel(const ConvArgs a) {
   constexpr int NT = (BM / MT) * (BN / MT);
@@ -195,6 +200,11 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? ((BM / MT) * 
       if (CPT * NT == BN || c < BN) {
 #pragma unroll
         for (int kk = 0; kk < PR; ++kk) {
+          if constexpr (!PADK) {
+            // columns past N (bzero) read image 0's window: valid memory, never stored
+            cp_async_4_zfill(smem_u32(bdst + kk * BN + c), bsrc[j] + d[kk], bzero[j]);
+            continue;
+          }
           const bool ok = d[kk] >= 0;
 #if IM2WIN_SIMT_NOCLAMP
           // ignore-src copies never touch the source: the address need not be valid
@@ -289,7 +299,11 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? ((BM / MT) * 
       cp_async_commit();
     }
     int slot = 0, pslot = STAGES - 1;
-    for (int kt = 0; kt < k_tiles; ++kt) {
+    // a last slab holding padded k runs after the loop over its real rows only (conv3: K = 147
+    // in 10 slabs of 16 would be 8% padded multiply-adds)
+    const bool k_tail = IM2WIN_SIMT_KTAIL && IM2WIN_SIMT_BRANCHLESS && VEC && PADK && a.K != a.Kp;
+    const int k_main = k_tail ? k_tiles - 1 : k_tiles;
+    for (int kt = 0; kt < k_main; ++kt) {
       cp_async_wait<STAGES - 2>();
       __syncthreads();
       const int pf = kt + STAGES - 1;
@@ -314,6 +328,30 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? ((BM / MT) * 
       cp_async_commit();
       slot = slot + 1 == STAGES ? 0 : slot + 1;
       pslot = pslot + 1 == STAGES ? 0 : pslot + 1;
+    }
+    if (k_tail) {
+      // slab k_tiles-1 sits in `slot` (the loop's redundant re-gathers went to other slots);
+      // skipping its zero rows changes no bits: acc never holds -0, so acc + rn(0*0) == acc
+      cp_async_wait<0>();
+      __syncthreads();
+      const int krem = a.K - (k_tiles - 1) * BK;
+      const float* as = As + slot * BK * BM;
+      const float* bs = Bs + slot * BK * BN;
+#pragma unroll 1
+      for (int kk = 0; kk < krem; ++kk) {
+        float fa[MT], fb[MT];
+#pragma unroll
+        for (int h = 0; h < HALVES; ++h) {
+          float4 av = *reinterpret_cast<const float4*>(as + kk * BM + h * (BM / 2) + ty * 4);
+          float4 bv = *reinterpret_cast<const float4*>(bs + kk * BN + h * (BN / 2) + tx * 4);
+          fa[4 * h] = av.x; fa[4 * h + 1] = av.y; fa[4 * h + 2] = av.z; fa[4 * h + 3] = av.w;
+          fb[4 * h] = bv.x; fb[4 * h + 1] = bv.y; fb[4 * h + 2] = bv.z; fb[4 * h + 3] = bv.w;
+        }
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < MT; ++j) acc[i][j] = mac<EXACT>(acc[i][j], fa[i], fb[j]);
+      }
     }
   }
 
@@ -514,6 +552,15 @@ static cudaError_t launch_cfg(const ConvArgs& a0, cudaStream_t stream) {
   size_t smem = static_cast<size_t>(STAGES) * BK * (BM + BN) * 4 + (sd ? static_cast<size_t>(a.Kp) * 4 : 0);
   auto kern = sd ? conv_simt_kernel<BM, BN, BK, STAGES, EXACT, VEC, MT, true>
                  : conv_simt_kernel<BM, BN, BK, STAGES, EXACT, VEC, MT, false>;
+#if IM2WIN_SIMT_BRANCHLESS && !defined(IM2WIN_SIMT_ALWAYS_PADK)
+  // production toggles, 8x8 micro-tiles: a K that fills whole slabs takes the predicate-free
+  // gather (measured, N=128: conv4/conv8 +2%, conv9/conv11 +2.4%; the 4x4-tile conv12 grid, one
+  // barrier-bound partial wave, lost 4% with it, so 4x4 tiles keep the predicated form)
+  if constexpr (STAGES > 1 && VEC && MT == 8) {
+    if (a.K == a.Kp) kern = sd ? conv_simt_kernel<BM, BN, BK, STAGES, EXACT, VEC, MT, true, false>
+                               : conv_simt_kernel<BM, BN, BK, STAGES, EXACT, VEC, MT, false, false>;
+  }
+#endif
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
