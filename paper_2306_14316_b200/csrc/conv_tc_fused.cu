@@ -462,7 +462,6 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  sms = tc_grid_sms(sms);
   const uint64_t tiles = static_cast<uint64_t>(a.n_tiles) * a.oh_tiles * a.ow_tiles * a.co_tiles;
   const uint32_t grid = tiles < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(tiles) : static_cast<uint32_t>(sms);
   if (ROW == 64)
@@ -548,14 +547,6 @@ int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c
     *err = "nchw_to_nhwc: dst must be 16-byte aligned and src 4-byte aligned";
     return 1;
   }
-  // overlap chunks: one tile per CTA (no grid stride) and SM-exclusive dynamic smem (unused)
-  // (48 KB per copy CTA including its static tile: no room left beside a >= 180 KB conv CTA)
-  const bool excl = im2win::tc::tc_copy_exclusive_smem() > 0;
-  auto xsmem = [&](const void* k) -> size_t {
-    cudaFuncAttributes fa{};
-    if (!excl || cudaFuncGetAttributes(&fa, k) != cudaSuccess) return 0;
-    return fa.sharedSizeBytes < 48 * 1024 ? 48 * 1024 - fa.sharedSizeBytes : 0;
-  };
   PadMap pm;
   pm.pad = static_cast<uint32_t>(pad);
   pm.wp = static_cast<uint32_t>(wp);
@@ -580,43 +571,37 @@ int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c
   }
   if (cp <= 8) {
     const uint64_t pixels = static_cast<uint64_t>(n) * hw;
-    const uint32_t g = static_cast<uint32_t>(std::min<uint64_t>((pixels + 255) / 256, excl ? (1u << 30) : 148 * 32));
-    const size_t xs = xsmem(bf16 ? reinterpret_cast<const void*>(im2win::tc::nchw_to_nhwc_small_kernel<true>)
-                                 : reinterpret_cast<const void*>(im2win::tc::nchw_to_nhwc_small_kernel<false>));
+    const uint32_t g = static_cast<uint32_t>(std::min<uint64_t>((pixels + 255) / 256, 148 * 32));
     if (bf16)
-      im2win::tc::nchw_to_nhwc_small_kernel<true><<<g, 256, xs, stream>>>(src, dst, static_cast<uint32_t>(c),
-                                                                          static_cast<uint32_t>(cp), hw, pixels, pm);
+      im2win::tc::nchw_to_nhwc_small_kernel<true><<<g, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
+                                                                         static_cast<uint32_t>(cp), hw, pixels, pm);
     else
-      im2win::tc::nchw_to_nhwc_small_kernel<false><<<g, 256, xs, stream>>>(src, dst, static_cast<uint32_t>(c),
-                                                                           static_cast<uint32_t>(cp), hw, pixels, pm);
+      im2win::tc::nchw_to_nhwc_small_kernel<false><<<g, 256, 0, stream>>>(src, dst, static_cast<uint32_t>(c),
+                                                                          static_cast<uint32_t>(cp), hw, pixels, pm);
     return done();
   }
   if (hw % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
     const int64_t wt = n * ((hw + 63) / 64) * ((cp + 63) / 64);
     if (wt < (1ll << 32)) {
-      const uint32_t g = static_cast<uint32_t>(std::min<int64_t>(wt, excl ? (1ll << 30) : 148 * 8));
-      const size_t xs = xsmem(bf16 ? reinterpret_cast<const void*>(im2win::tc::nchw_to_nhwc_wide_kernel<true>)
-                                   : reinterpret_cast<const void*>(im2win::tc::nchw_to_nhwc_wide_kernel<false>));
+      const uint32_t g = static_cast<uint32_t>(std::min<int64_t>(wt, 148 * 8));
       if (bf16)
-        im2win::tc::nchw_to_nhwc_wide_kernel<true><<<g, 256, xs, stream>>>(
+        im2win::tc::nchw_to_nhwc_wide_kernel<true><<<g, 256, 0, stream>>>(
             src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(cp), static_cast<uint32_t>(hw),
             static_cast<uint32_t>((hw + 63) / 64), static_cast<uint32_t>((cp + 63) / 64), static_cast<uint32_t>(wt), pm);
       else
-        im2win::tc::nchw_to_nhwc_wide_kernel<false><<<g, 256, xs, stream>>>(
+        im2win::tc::nchw_to_nhwc_wide_kernel<false><<<g, 256, 0, stream>>>(
             src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(cp), static_cast<uint32_t>(hw),
             static_cast<uint32_t>((hw + 63) / 64), static_cast<uint32_t>((cp + 63) / 64), static_cast<uint32_t>(wt), pm);
       return done();
     }
   }
-  const uint32_t grid = static_cast<uint32_t>(excl ? total : total < 148 * 16 ? total : 148 * 16);
-  const size_t xs = xsmem(bf16 ? reinterpret_cast<const void*>(im2win::tc::nchw_to_nhwc_kernel<true>)
-                               : reinterpret_cast<const void*>(im2win::tc::nchw_to_nhwc_kernel<false>));
+  const uint32_t grid = static_cast<uint32_t>(total < 148 * 16 ? total : 148 * 16);
   if (bf16)
-    im2win::tc::nchw_to_nhwc_kernel<true><<<grid, 256, xs, stream>>>(
+    im2win::tc::nchw_to_nhwc_kernel<true><<<grid, 256, 0, stream>>>(
         src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(cp), static_cast<uint32_t>(hw),
         static_cast<uint32_t>(hw_tiles), static_cast<uint32_t>(c_tiles), static_cast<uint32_t>(total), pm);
   else
-    im2win::tc::nchw_to_nhwc_kernel<false><<<grid, 256, xs, stream>>>(
+    im2win::tc::nchw_to_nhwc_kernel<false><<<grid, 256, 0, stream>>>(
         src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(cp), static_cast<uint32_t>(hw),
         static_cast<uint32_t>(hw_tiles), static_cast<uint32_t>(c_tiles), static_cast<uint32_t>(total), pm);
   return done();
@@ -652,83 +637,6 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
 
 int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n,
                                 int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride,
-                                int bf16, const float* feed_src, cudaStream_t stream, const char** err);
-
-namespace {
-
-// Chunked copy/conv overlap for large batches.  The channels-last copy is HBM bound and the conv
-// kernels are shared-memory bound, but run in one SM they contend (the in-kernel feed, §8 of
-// DESIGN.md); on disjoint SMs they do not.  The batch is cut into chunks: the copy of chunk i+1
-// runs on `reserve` SMs (copy CTAs ask for SM-exclusive shared memory, on a low-priority stream)
-// while the conv of chunk i runs as a persistent grid on the others (high-priority stream); the
-// last chunk's conv takes every SM.  Fork/join through events on the caller's stream; each output
-// image is computed by the same kernel and tile as without chunks, so the bits do not change.
-struct OverlapCtx {
-  cudaStream_t conv = nullptr, copy = nullptr;
-  cudaEvent_t ev[66] = {};
-  bool ok = false;
-};
-
-int launch_overlapped(const float* src, void* x_cl, const float* flt, float* out, void* workspace, int64_t n,
-                      int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride, int bf16,
-                      int64_t chunk, int reserve, cudaStream_t stream, const char** err) {
-  using namespace im2win::tc;
-  static thread_local OverlapCtx ctx[16];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  OverlapCtx& c = ctx[dev & 15];
-  auto fail = [&](cudaError_t e) {
-    *err = cudaGetErrorString(e);
-    return 2;
-  };
-  if (!c.ok) {
-    int least = 0, greatest = 0;
-    cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    cudaError_t e = cudaStreamCreateWithPriority(&c.conv, cudaStreamNonBlocking, greatest);
-    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c.copy, cudaStreamNonBlocking, least);
-    for (int i = 0; i < 66 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&c.ev[i], cudaEventDisableTiming);
-    if (e != cudaSuccess) return fail(e);
-    c.ok = true;
-  }
-  const int64_t chunks = (n + chunk - 1) / chunk;  // <= 63 (caller)
-  const int64_t cp = im2win_nhwc_channel_pitch(c_in, bf16);
-  const int64_t h_out = (h - h_f) / stride + 1, w_out = (w - w_f) / stride + 1;
-  const int64_t img_in = c_in * h * w, img_cl = h * w * cp * (bf16 ? 2 : 4), img_out = c_out * h_out * w_out;
-  cudaError_t e = cudaEventRecord(c.ev[0], stream);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(c.copy, c.ev[0], 0);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(c.conv, c.ev[0], 0);
-  if (e != cudaSuccess) return fail(e);
-  for (int64_t i = 0; i < chunks; ++i) {
-    const int64_t i0 = i * chunk, ni = std::min(chunk, n - i0);
-    // the first chunk's copy has the GPU to itself: plain grid-stride launch
-    tc_copy_exclusive_smem() = i == 0 ? 0 : 32 * 1024;
-    const int rc = im2win_launch_nchw_to_nhwc(src + i0 * img_in, static_cast<char*>(x_cl) + i0 * img_cl, ni, c_in, h,
-                                              w, bf16, 0, c.copy, err);
-    tc_copy_exclusive_smem() = 0;
-    if (rc) return rc;
-    if ((e = cudaEventRecord(c.ev[1 + i], c.copy)) != cudaSuccess) return fail(e);
-  }
-  for (int64_t i = 0; i < chunks; ++i) {
-    const int64_t i0 = i * chunk, ni = std::min(chunk, n - i0);
-    if ((e = cudaStreamWaitEvent(c.conv, c.ev[1 + i], 0)) != cudaSuccess) return fail(e);
-    tc_sm_reserve() = i + 1 < chunks ? reserve : 0;
-    const int rc = im2win_launch_conv_tc_fused(static_cast<char*>(x_cl) + i0 * img_cl, flt, out + i0 * img_out,
-                                               workspace, ni, c_in, h, w, c_out, h_f, w_f, stride, bf16, nullptr,
-                                               c.conv, err);
-    tc_sm_reserve() = 0;
-    if (rc) return rc;
-  }
-  e = cudaEventRecord(c.ev[64], c.conv);
-  if (e == cudaSuccess) e = cudaEventRecord(c.ev[65], c.copy);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, c.ev[64], 0);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, c.ev[65], 0);
-  return e == cudaSuccess ? 0 : fail(e);
-}
-
-}  // namespace
-
-int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, void* workspace, int64_t n,
-                                int64_t c_in, int64_t h, int64_t w, int64_t c_out, int h_f, int w_f, int stride,
                                 int bf16, const float* feed_src, cudaStream_t stream, const char** err) {
   using namespace im2win::tc;
   // feed_src != nullptr: x_cl is scratch, produced from the NCHW input inside the conv kernel
@@ -747,17 +655,6 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
     const int64_t h_o = (h - h_f) / stride + 1, w_o = (w - w_f) / stride + 1;
     const double r = static_cast<double>(c_out * h_o * w_o) / static_cast<double>(c_in * h * w);
     if (mode == 0 || (mode == 1 && (r > 0.5 || n > 256))) {
-      // large batches: chunked copy/conv overlap on disjoint SMs (IM2WIN_OVERLAP: images per chunk,
-      // 0 off; IM2WIN_OVERLAP_SMS: SMs the copy runs on)
-      const char* oe = getenv("IM2WIN_OVERLAP");
-      const int64_t chunk = oe ? atoll(oe) : 0;
-      const char* se = getenv("IM2WIN_OVERLAP_SMS");
-      const int reserve = se ? atoi(se) : 24;
-      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-      cudaStreamIsCapturing(stream, &cap);
-      if (chunk > 0 && n >= 2 * chunk && (n + chunk - 1) / chunk <= 63 && cap == cudaStreamCaptureStatusNone)
-        return launch_overlapped(feed_src, const_cast<void*>(x_cl), flt, out, workspace, n, c_in, h, w, c_out, h_f,
-                                 w_f, stride, bf16, chunk, reserve, stream, err);
       const int rc = im2win_launch_nchw_to_nhwc(feed_src, const_cast<void*>(x_cl), n, c_in, h, w, bf16, 0, stream, err);
       if (rc) return rc;
       feed_src = nullptr;

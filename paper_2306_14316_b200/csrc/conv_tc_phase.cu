@@ -435,7 +435,6 @@ static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  sms = tc_grid_sms(sms);
   const uint64_t items = static_cast<uint64_t>(a.pairs) * a.co_tiles;
   uint32_t grid = items < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(items) : static_cast<uint32_t>(sms);
   if constexpr (PAIR) {

@@ -314,7 +314,6 @@ static int launch_shift(ShiftArgs a, const void* x_cl, const void* packed, int64
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  sms = tc_grid_sms(sms);
   const uint64_t tiles = static_cast<uint64_t>(a.n_tiles) * a.oh_tiles * a.ow_tiles * a.co_tiles;
   const uint32_t grid = tiles < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(tiles) : static_cast<uint32_t>(sms);
   im2win_note_kernel(RB ? "conv_tc_shift_kernel (window shift, filter resident)" : "conv_tc_shift_kernel (window shift)");

@@ -472,23 +472,6 @@ inline NhwcFeed feed_for(const NhwcFeed& f, uint64_t grid, uint64_t items) {
 // Launch of a TMA-fed conv kernel: with a feed, the extra converter warps and a cooperative
 // launch (the CTAs wait on each other's feed units, so all must be co-resident).
 // cluster = 2: CTA pairs (cta_group::2 kernels).
-// Chunked copy/conv overlap (im2win_launch_conv_tc_fused): SMs withheld from the persistent conv
-// grids while the channels-last copy of the next chunk runs on them (0 = every SM), and the dynamic
-// shared memory the copy kernels then request so that no copy CTA fits next to a conv CTA
-// (the conv kernels hold 190-220 KB): the two stay on disjoint SMs.  Per host thread.
-inline int& tc_sm_reserve() {
-  static thread_local int v = 0;
-  return v;
-}
-inline int tc_grid_sms(int sms) {
-  const int r = tc_sm_reserve();
-  return r > 0 && sms - r >= 8 ? sms - r : sms;
-}
-inline size_t& tc_copy_exclusive_smem() {
-  static thread_local size_t v = 0;
-  return v;
-}
-
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_tc_kernel(void (*kern)(KArgs...), uint32_t grid, size_t smem, cudaStream_t stream,
                                     bool feed, int cluster, Args&&... args) {
