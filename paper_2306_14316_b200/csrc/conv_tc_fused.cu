@@ -492,103 +492,6 @@ int64_t im2win_nhwc_channel_pitch(int64_t c, int bf16) {
 
 namespace im2win {
 namespace tc {
-// Window image for few-channel inputs: row (img, oh, ow) holds that output pixel's whole window
-// W[k] = X[img][c][oh*s + fh][ow*s + fw], k = (c*Hf + fh)*Wf + fw (the filter's own flattening),
-// zero-padded to the channel-pitch kp of K channels, converted like the channels-last copy (bf16
-// round to nearest / raw fp32 for tf32).  A stride-1 1x1 conv over it with C' = K is the layer: the
-// 3-channel layers' windows then arrive as one K-row per pixel instead of Hf rows of Wf*C_pad
-// mostly-padding elements.  One item = one 16-byte group of consecutive k (8 bf16 / 4 fp32) of one
-// pixel; the groups of a pixel are adjacent lanes, so a warp's stores cover contiguous pixel rows.
-template <bool BF16>
-__global__ void __launch_bounds__(256) nchw_to_windows_kernel(const float* __restrict__ src, void* __restrict__ dst,
-                                                              uint32_t c_in, uint32_t h, uint32_t w, uint32_t h_f,
-                                                              uint32_t w_f, uint32_t stride, uint32_t w_out,
-                                                              uint32_t hw_out, uint32_t k_real, uint32_t kp,
-                                                              uint64_t items) {
-  constexpr uint32_t G = BF16 ? 8 : 4;
-  const uint32_t kg_n = kp / G, fhw = h_f * w_f;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < items;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t px = i / kg_n;
-    const uint32_t k0 = static_cast<uint32_t>(i % kg_n) * G;
-    const uint64_t img = px / hw_out;
-    const uint32_t p = static_cast<uint32_t>(px % hw_out);
-    const uint32_t oh = p / w_out, ow = p % w_out;
-    const float* s0 = src + img * c_in * h * w + static_cast<uint64_t>(oh * stride) * w + ow * stride;
-    uint32_t c = k0 / fhw, r = k0 % fhw;
-    uint32_t fh = r / w_f, fw = r % w_f;
-    float v[G];
-#pragma unroll
-    for (int j = 0; j < static_cast<int>(G); ++j) {
-      v[j] = (k0 + j < k_real) ? __ldg(s0 + (static_cast<uint64_t>(c) * h + fh) * w + fw) : 0.0f;
-      if (++fw == w_f) {
-        fw = 0;
-        if (++fh == h_f) {
-          fh = 0;
-          ++c;
-        }
-      }
-    }
-    if constexpr (BF16) {
-      uint4 q;
-      q.x = pack_bf16x2(v[0], v[1]);
-      q.y = pack_bf16x2(v[2], v[3]);
-      q.z = pack_bf16x2(v[4], v[5]);
-      q.w = pack_bf16x2(v[6], v[7]);
-      __stcs(reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dst) + px * kp + k0), q);
-    } else {
-      __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + px * kp + k0),
-             make_float4(v[0], v[1], v[2], v[3]));
-    }
-  }
-}
-}  // namespace tc
-}  // namespace im2win
-
-// Window-image path (im2win_launch_conv_tc_fused): the window rows' pitch is the channels-last
-// pitch of K = C*Hf*Wf channels, as the 1x1 conv over them expects.
-static int64_t windows_pitch(int64_t c_in, int h_f, int w_f, int bf16) {
-  return im2win_nhwc_channel_pitch(c_in * h_f * w_f, bf16);
-}
-
-// Bytes of the window image for n images (0 when the path does not apply).
-size_t im2win_tc_windows_bytes(int64_t n, int64_t c_in, int64_t h, int64_t w, int h_f, int w_f, int stride, int bf16) {
-  const int64_t h_out = (h - h_f) / stride + 1, w_out = (w - w_f) / stride + 1;
-  return static_cast<size_t>(n * h_out * w_out * windows_pitch(c_in, h_f, w_f, bf16)) * (bf16 ? 2 : 4);
-}
-
-static int launch_nchw_to_windows(const float* src, void* dst, int64_t n, int64_t c_in, int64_t h, int64_t w, int h_f,
-                                  int w_f, int stride, int bf16, cudaStream_t stream, const char** err) {
-  const int64_t h_out = (h - h_f) / stride + 1, w_out = (w - w_f) / stride + 1;
-  const int64_t kp = windows_pitch(c_in, h_f, w_f, bf16);
-  const uint64_t items = static_cast<uint64_t>(n * h_out * w_out) * (kp / (bf16 ? 8 : 4));
-  if (c_in * h * w >= (1ll << 31) || h_out * w_out >= (1ll << 31)) {
-    *err = "nchw_to_windows: extents exceed the kernel's index range";
-    return 1;
-  }
-  const uint32_t g = static_cast<uint32_t>(std::min<uint64_t>((items + 255) / 256, 148 * 16));
-  const uint32_t args[] = {static_cast<uint32_t>(c_in), static_cast<uint32_t>(h), static_cast<uint32_t>(w),
-                           static_cast<uint32_t>(h_f), static_cast<uint32_t>(w_f), static_cast<uint32_t>(stride),
-                           static_cast<uint32_t>(w_out), static_cast<uint32_t>(h_out * w_out),
-                           static_cast<uint32_t>(c_in * h_f * w_f), static_cast<uint32_t>(kp)};
-  if (bf16)
-    im2win::tc::nchw_to_windows_kernel<true><<<g, 256, 0, stream>>>(src, dst, args[0], args[1], args[2], args[3],
-                                                                    args[4], args[5], args[6], args[7], args[8],
-                                                                    args[9], items);
-  else
-    im2win::tc::nchw_to_windows_kernel<false><<<g, 256, 0, stream>>>(src, dst, args[0], args[1], args[2], args[3],
-                                                                     args[4], args[5], args[6], args[7], args[8],
-                                                                     args[9], items);
-  const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    *err = cudaGetErrorString(e);
-    return 2;
-  }
-  return 0;
-}
-
-namespace im2win {
-namespace tc {
 // The feed warps' code alone (no conv): tools/feed_ab.py measures its copy rate (IM2WIN_FEED_PROBE=1).
 template <bool BF16>
 __global__ void __launch_bounds__(32 * kFeedWarps) nhwc_feed_only_kernel(const NhwcFeed f) {
@@ -740,18 +643,6 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
   // (counters at the end of the workspace, see im2win_tc_feed_counters)
   NhwcFeed feed{};
   if (feed_src) {
-    // few-channel inputs: window image + 1x1 conv (IM2WIN_WINDOWS: 0 off, 1 auto, 2 always)
-    const char* we = getenv("IM2WIN_WINDOWS");
-    const int wmode = we ? atoi(we) : 0;
-    if (wmode == 2 || (wmode == 1 && c_in <= 4)) {
-      const int rc = launch_nchw_to_windows(feed_src, const_cast<void*>(x_cl), n, c_in, h, w, h_f, w_f, stride, bf16,
-                                            stream, err);
-      if (rc) return rc;
-      const int64_t h_o = (h - h_f) / stride + 1, w_o = (w - w_f) / stride + 1;
-      // the filter [Co][C][Hf][Wf] is already [Co][K][1][1]
-      return im2win_launch_conv_tc_fused(x_cl, flt, out, workspace, n, c_in * h_f * w_f, h_o, w_o, c_out, 1, 1, 1,
-                                         bf16, nullptr, stream, err);
-    }
     // In-kernel feed or a copy kernel first.  Measured (tools/feed_ab.py): the feed warps share the
     // SM's L1/shared-memory datapath and HBM with the conv, so overlap pays only where the conv's
     // own traffic is light next to the input -- output/input elements r = (Co*Ho*Wo)/(C*H*W) <= 0.5
