@@ -188,7 +188,6 @@ struct FusedArgs {
   uint32_t ow_tiles, oh_tiles, n_tiles, co_tiles;
   uint32_t k_slabs, fh_slabs;  // k_slabs = Hf * fh_slabs
   uint32_t group;              // consecutive tiles per CTA visit (the pieces of an output row together)
-  uint32_t staged;             // epilogue stages the tile in smem and writes 128-byte-aligned lines
 };
 
 // This CTA's tiles: runs of `group` consecutive tiles, runs strided by the grid (group 1 =
@@ -331,60 +330,6 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
   } else if (warp >= 4 + kEpiWarps) {
     if (feed.src)
       nhwc_feed_run<BF16>(feed, lane, blockIdx.x * kFeedWarps + (warp - 4 - kEpiWarps), gridDim.x * kFeedWarps);
-  } else if (warp >= 4 && a.staged) {
-    // Staged epilogue: the tile goes TMEM -> smem [co][pixel], then each output row run (one
-    // channel's pixels of the tile, contiguous in NCHW) is written as whole 128-byte-aligned lines,
-    // lane = float of the line.  The lane = pixel stores of the plain epilogue start wherever the
-    // tile's pixels fall, so most warp stores split over two lines: twice the L1 -> L2 write
-    // requests, the interface conv7's plain epilogue keeps 80% busy (ncu).
-    const int quarter = warp % 4;
-    const int j_lo = ((warp - 4) / 4) * (N / 2);
-    const uint32_t r = quarter * 32 + lane;
-    const uint32_t ew = warp - 4;  // 0 .. kEpiWarps-1
-    float* stg = reinterpret_cast<float*>(smem + STAGES * kStageBytes);  // [N][kTileM]
-    const bool full_rows = a.box_w == a.w_out;  // a run covers box_h whole rows
-    const uint32_t run_rows = full_rows ? 1u : a.box_h;
-    const uint32_t runs = static_cast<uint32_t>(N) * a.box_n * run_rows;
-    uint32_t acc = 0, acc_phase = 0;
-    for (TileWalk w(a.group); w.t < total_tiles; w.next()) {
-      const uint32_t t = w.t;
-      const uint32_t co_blk = t % a.co_tiles;
-      uint32_t pt = t / a.co_tiles;
-      const uint32_t ow0 = (pt % a.ow_tiles) * a.box_w;
-      pt /= a.ow_tiles;
-      const uint32_t oh0 = (pt % a.oh_tiles) * a.box_h;
-      const uint32_t n0 = (pt / a.oh_tiles) * a.box_n;
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
-      asm volatile("bar.sync 1, %0;\n" ::"r"(kEpiWarps * 32) : "memory");  // previous tile's runs written
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * N;
-#pragma unroll
-      for (int jj = 0; jj < N / 2; jj += 16) {
-        const int j0 = j_lo + jj;
-        uint32_t v[16];
-        tmem_ld16(taddr + j0, v);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) stg[(j0 + q) * kTileM + r] = __uint_as_float(v[q]);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      asm volatile("bar.sync 1, %0;\n" ::"r"(kEpiWarps * 32) : "memory");  // tile staged
-      for (uint32_t run = ew; run < runs; run += kEpiWarps) {
-        const uint32_t co_l = run % N, rest = run / N;
-        const uint32_t row = rest % run_rows, n_l = rest / run_rows;
-        const uint32_t co = co_blk * N + co_l, img = n0 + n_l, oh = oh0 + row;
-        if (co >= a.co || img >= a.n_img || oh >= a.h_out) continue;
-        const uint32_t len = full_rows ? min(a.box_h, a.h_out - oh0) * a.w_out : min(a.box_w, a.w_out - ow0);
-        const int64_t g = (static_cast<int64_t>(img) * a.co + co) * a.hw + static_cast<int64_t>(oh) * a.w_out + ow0;
-        const float* src = stg + co_l * kTileM + (n_l * a.box_h + row) * a.box_w;
-        for (int64_t b = g & ~int64_t(31); b < g + len; b += 32) {
-          const int64_t idx = b + lane;
-          if (idx >= g && idx < g + len) st_out(a.out + idx, src[idx - g]);
-        }
-      }
-    }
   } else if (warp >= 4) {
     // kEpiWarps epilogue warps: warp w reads TMEM lane quarter w % 4 and column half (w - 4) / 4
     const int quarter = warp % 4;
@@ -507,14 +452,7 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
     a.group = static_cast<uint32_t>(g < 1 ? 1 : g);
   }
   const size_t rb = RB ? static_cast<size_t>(a.k_slabs) * N * ROW : 0;
-  size_t smem = rb + static_cast<size_t>(STAGES) * (kTileM + (RB ? 0 : N)) * ROW + 1024;
-  {
-    // staged epilogue (IM2WIN_STAGED_EPI: 0 off, 1 on where the [N][128] fp32 tile fits)
-    const char* se = getenv("IM2WIN_STAGED_EPI");
-    const size_t stg = static_cast<size_t>(N) * kTileM * 4;
-    a.staged = (se && atoi(se) > 0 && smem + stg <= 227 * 1024) ? 1u : 0u;
-    if (a.staged) smem += stg;
-  }
+  const size_t smem = rb + static_cast<size_t>(STAGES) * (kTileM + (RB ? 0 : N)) * ROW + 1024;
   auto kern = conv_tc_fused_kernel<BF16, N, STAGES, RB, ROW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) {
