@@ -934,9 +934,10 @@ def test_nchw_direct_equals_window_path_all_layers(variant, monkeypatch, layer_g
 
 
 def test_nchw_direct_large_batch_sampled_images():
-    """NCHW-direct FP32-exact at N=128 (conv4, conv7 small-K, conv12 4x4 tiles, conv1 96-wide
-    tiles and tail split): sampled images bitwise equal to the oracle."""
-    for name in ("conv4", "conv7", "conv12", "conv1"):
+    """NCHW-direct FP32-exact at N=128 (conv4 and conv8: K in whole slabs, the predicate-free
+    gather; conv3: padded last K slab computed over its real rows; conv7 small-K, conv12 4x4 tiles,
+    conv1 96-wide tiles and tail split): sampled images bitwise equal to the oracle."""
+    for name in ("conv4", "conv8", "conv3", "conv7", "conv12", "conv1"):
         cfg = replace(BENCHMARKS[name], batch=128)
         g = torch.Generator(device=DEV).manual_seed(77)
         x = torch.randn((128, cfg.c_in, cfg.h_in, cfg.w_in), device=DEV, generator=g)
