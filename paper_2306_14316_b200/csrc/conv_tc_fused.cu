@@ -77,6 +77,70 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restri
   }
 }
 
+// Small-image variant (H*W <= 256 and not a multiple of 4, e.g. 7x7: conv12): a CTA moves a
+// 32-channel slab of one image, which is one contiguous run of 32*H*W floats -- loaded with
+// 16-byte loads when the image is 16-byte aligned -- transposed in smem (odd row pitch) and
+// written as whole 128-byte (fp32) / 64-byte (bf16) pixel rows.  The 32x32 generic kernel moves
+// such images at ~3.3 TB/s: half of its second pixel tile is empty and its loads are scalar.
+template <bool BF16>
+__global__ void __launch_bounds__(128) nchw_to_nhwc_block_kernel(const float* __restrict__ src, void* __restrict__ dst,
+                                                                 uint32_t c_in, uint32_t c_pad, uint32_t hw,
+                                                                 uint32_t c_tiles, uint32_t total, uint32_t vec,
+                                                                 const PadMap pm) {
+  extern __shared__ float tile[];  // [32][pitch]: small, so many CTAs (and their loads) per SM
+  const uint32_t pitch = hw | 1u;
+  constexpr uint32_t G = BF16 ? 8 : 4;  // channels per 16-byte store
+  for (uint32_t b = blockIdx.x; b < total; b += gridDim.x) {
+    const uint32_t ct = b % c_tiles, img = b / c_tiles;
+    const uint32_t c0 = ct * 32;
+    const uint32_t nc = min(32u, c_in - c0);
+    const float* s = src + (static_cast<uint64_t>(img) * c_in + c0) * hw;
+    const uint32_t cnt = nc * hw;
+    if (vec) {
+      for (uint32_t q = threadIdx.x; q < cnt / 4; q += blockDim.x) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(s) + q);
+        const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t f = 4 * q + j, c = f / hw;
+          tile[c * pitch + (f - c * hw)] = e[j];
+        }
+      }
+    } else {
+      for (uint32_t f = threadIdx.x; f < cnt; f += blockDim.x) {
+        const uint32_t c = f / hw;
+        tile[c * pitch + (f - c * hw)] = __ldg(s + f);
+      }
+    }
+    __syncthreads();
+    // write: 32/G threads per pixel, G channels each; channels >= c_in (pitch padding) are zeros
+    const uint32_t per = 32 / G;
+    const uint32_t groups = min(per, (c_pad - c0 + G - 1) / G);
+    for (uint32_t i = threadIdx.x; i < hw * per; i += blockDim.x) {
+      const uint32_t p = i / per, g = i % per;
+      if (g >= groups) continue;
+      float v[G];
+#pragma unroll
+      for (uint32_t j = 0; j < G; ++j) {
+        const uint32_t c = g * G + j;
+        v[j] = c < nc ? tile[c * pitch + p] : 0.0f;
+      }
+      const uint64_t o = pm.pixel(img, p) * c_pad + c0 + g * G;
+      if constexpr (BF16) {
+        uint4 q;
+        q.x = pack_bf16x2(v[0], v[1]);
+        q.y = pack_bf16x2(v[2], v[3]);
+        q.z = pack_bf16x2(v[4], v[5]);
+        q.w = pack_bf16x2(v[6], v[7]);
+        __stcs(reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dst) + o), q);
+      } else {
+        __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + o), make_float4(v[0], v[1], v[2], v[3]));
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Wide-tile variant (c_pad > 8, Ho*Wo % 4 == 0): a CTA moves a 64-channel x 64-pixel
 // tile per iteration -- four 16-byte loads per thread in flight, a padded smem
 // transpose (row pitch 65 floats), and 16-byte channels-last stores (4 fp32 or 8 bf16
@@ -592,6 +656,24 @@ int im2win_launch_nchw_to_nhwc(const float* src, void* dst, int64_t n, int64_t c
         im2win::tc::nchw_to_nhwc_wide_kernel<false><<<g, 256, 0, stream>>>(
             src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(cp), static_cast<uint32_t>(hw),
             static_cast<uint32_t>((hw + 63) / 64), static_cast<uint32_t>((cp + 63) / 64), static_cast<uint32_t>(wt), pm);
+      return done();
+    }
+  }
+  const char* cbe = getenv("IM2WIN_COPY_BLOCK");  // 0: the 32x32 generic kernel (A/B)
+  if (hw <= 256 && !(cbe && atoi(cbe) == 0)) {
+    const int64_t bt = n * ((c + 31) / 32);
+    if (bt < (1ll << 32)) {
+      const uint32_t g = static_cast<uint32_t>(std::min<int64_t>(bt, 148 * 16));
+      const uint32_t vec = ((c * hw) % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) ? 1u : 0u;
+      const size_t sm = static_cast<size_t>(32) * (hw | 1) * 4;
+      if (bf16)
+        im2win::tc::nchw_to_nhwc_block_kernel<true><<<g, 128, sm, stream>>>(
+            src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(cp), static_cast<uint32_t>(hw),
+            static_cast<uint32_t>((c + 31) / 32), static_cast<uint32_t>(bt), vec, pm);
+      else
+        im2win::tc::nchw_to_nhwc_block_kernel<false><<<g, 128, sm, stream>>>(
+            src, dst, static_cast<uint32_t>(c), static_cast<uint32_t>(cp), static_cast<uint32_t>(hw),
+            static_cast<uint32_t>((c + 31) / 32), static_cast<uint32_t>(bt), vec, pm);
       return done();
     }
   }

@@ -976,3 +976,29 @@ def test_tc_fused_64byte_rows(variant, monkeypatch, layer_goldens):
     inp, flt = cases[0][0]
     pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant, tc_path="fused")
     assert "64-byte rows" in _lib.last_kernel()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_nhwc_copy_small_image_block_kernel(dtype, monkeypatch):
+    """The channels-last copy of small images whose H*W is not a multiple of 4 (7x7: conv12) goes
+    through the 32-channel block kernel: equal to the 32x32 generic kernel and to a torch
+    permute + pad + cast, for odd channel counts, a channel tail, unaligned images and a border."""
+    from paper_2306_14316_b200.kernels import nhwc_into
+
+    q = 8 if dtype == torch.bfloat16 else 4
+    g = torch.Generator(device=DEV).manual_seed(21)
+    for (n, c, h, w, pad) in [(3, 512, 7, 7, 0), (2, 33, 5, 9, 0), (2, 9, 15, 15, 1), (1, 70, 13, 11, 0),
+                              (4, 16, 3, 3, 2)]:
+        x = torch.randn((n, c, h, w), device=DEV, generator=g)
+        pitch = -(-c // q) * q
+        got = torch.full((n, h + 2 * pad, w + 2 * pad, pitch), 7.0, device=DEV, dtype=dtype)
+        ref = torch.full_like(got, 7.0)
+        nhwc_into(x, got, pad)
+        monkeypatch.setenv("IM2WIN_COPY_BLOCK", "0")
+        nhwc_into(x, ref, pad)
+        monkeypatch.delenv("IM2WIN_COPY_BLOCK")
+        want = torch.zeros_like(got)
+        want[:, pad:pad + h, pad:pad + w, :c] = x.permute(0, 2, 3, 1).to(dtype)
+        assert torch.equal(got.view(torch.int16 if dtype == torch.bfloat16 else torch.int32),
+                           ref.view(torch.int16 if dtype == torch.bfloat16 else torch.int32)), (n, c, h, w, pad)
+        assert torch.equal(got.float(), want.float()), (n, c, h, w, pad)
