@@ -9,6 +9,8 @@
 // Records which kernel the last library call on this host thread launched
 // (im2win_last_kernel(); capi.cu).  Static strings only.
 void im2win_note_kernel(const char* name);
+// relabel the call's kernel without counting a launch (a call made of several launches)
+void im2win_label_kernel(const char* name);
 
 namespace im2win {
 

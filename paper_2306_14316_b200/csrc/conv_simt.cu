@@ -736,6 +736,7 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
         ConvArgs at = a;
         at.n_base = n_main;
         e = dispatch(tail_cfg, at);
+        im2win_label_kernel("conv_simt_kernel (8x8 micro-tiles, 4x4-tile tail launch)");
       }
     } else {
       e = dispatch(cfg, a);
