@@ -42,7 +42,12 @@ constexpr int kPhRows = 136;  // 128 MMA rows + up to 8 rows of shift
 // tiles and half of each filter tap (N/2 rows), so the per-SM shared-memory operand bytes per
 // MMA drop from (128 + N) to (128 + N/2) rows and the filter's L2->SM traffic halves.  Work
 // items are then 2*MT pixel tiles (MT per CTA).  Rank 0 issues the MMAs.
-template <bool BF16, int N, int STAGES, int TAPS, int MT, bool PAIR>
+// TN2: two taps per MMA (Co <= 64): B rows 0-63 are tap q, rows 64-127 tap q+1 -- the ring's
+// consecutive tap tiles -- both against the A tile shifted for tap q, so D columns 64-127 hold
+// tap q+1 one pixel early and the epilogue adds D[p][co] + D[p+1][64+co].  A 128x128x16 UMMA
+// reads 8 KB of operands for twice the work of a 128x64x16 one (6 KB): 64 vs 2 x 48 cycles
+// (tools/probes/umma_rate.cu).  An odd last tap runs as a plain N=64 MMA into columns 0-63.
+template <bool BF16, int N, int STAGES, int TAPS, int MT, bool PAIR, bool TN2 = false>
 __global__ void __launch_bounds__(kTcThreadsFeed, 1)
     conv_tc_phase_kernel(const PhaseArgs a, const __grid_constant__ CUtensorMap tmap_a0,
                          const __grid_constant__ CUtensorMap tmap_a1, const __grid_constant__ CUtensorMap tmap_b,
@@ -54,11 +59,14 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
   constexpr uint32_t kStageBytes = kABytes + TAPS * kBTap;
   constexpr int kBK = BF16 ? 64 : 32;
   constexpr int kUK = BF16 ? 16 : 8;
-  constexpr uint32_t kTmemCols = (2 * MT * N <= 128) ? 128 : (2 * MT * N <= 256 ? 256 : 512);
+  constexpr int kAccN = TN2 ? 2 * N : N;  // TMEM columns per pixel tile
+  constexpr uint32_t kTmemCols = (2 * MT * kAccN <= 128) ? 128 : (2 * MT * kAccN <= 256 ? 256 : 512);
   constexpr uint32_t kIdesc = instr_desc_m<BF16, N, PAIR ? 256 : 128>();
+  constexpr uint32_t kIdesc2 = instr_desc_m<BF16, 2 * N, 128>();
+  static_assert(!TN2 || (!PAIR && N == 64), "tap pairs: single CTA, Co tile 64");
   constexpr uint32_t kCtas = PAIR ? 2 : 1;
   static_assert(kATile % 1024 == 0 && kBTap % 1024 == 0, "tiles must keep 1024 B alignment");
-  static_assert(2 * MT * N <= 512, "TMEM holds 512 fp32 columns");
+  static_assert(2 * MT * kAccN <= 512, "TMEM holds 512 fp32 columns");
 
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[STAGES];
@@ -66,6 +74,8 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
   __shared__ __align__(8) uint64_t tfull_bar[2];
   __shared__ __align__(8) uint64_t tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
+  // TN2: each quarter warp's first-row tap-(q+1) columns, for the warp of the quarter before it
+  __shared__ float xch[TN2 ? 2 * MT * 2 * 4 * 32 : 1];
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x / 32;
@@ -190,7 +200,7 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
         for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
           mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
           tc_fence_after();
-          const uint32_t tmem_d = tmem_base + acc * (MT * N);
+          const uint32_t tmem_d = tmem_base + acc * (MT * kAccN);
           for (uint32_t ki = 0; ki < a.k_iters; ++ki) {
             const uint32_t r = (ki / a.c_slabs) % s;
             const uint32_t nq = (a.w_f - r + s - 1) / s;
@@ -198,6 +208,33 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
             tc_fence_after();
             const uint32_t abase = smem_u32(smem + stage * kStageBytes);
             const uint32_t bbase = abase + kABytes;
+            if constexpr (TN2) {
+#pragma unroll
+              for (int q = 0; q < TAPS; q += 2) {
+                if (q + 1 < static_cast<int>(nq)) {
+#pragma unroll
+                  for (int kk = 0; kk < kBK / kUK; ++kk) {
+                    const uint64_t bd = smem_desc_sw128(bbase + q * kBTap + kk * 32);  // taps q, q+1: 128 rows
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt)
+                      mma<BF16>(tmem_d + mt * kAccN, smem_desc_sw128(abase + mt * kATile + q * kRowBytes + kk * 32),
+                                bd, kIdesc2, (ki | q | kk) != 0);
+                  }
+                } else if (q < static_cast<int>(nq)) {
+#pragma unroll
+                  for (int kk = 0; kk < kBK / kUK; ++kk) {
+                    const uint64_t bd = smem_desc_sw128(bbase + q * kBTap + kk * 32);
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt)
+                      mma<BF16>(tmem_d + mt * kAccN, smem_desc_sw128(abase + mt * kATile + q * kRowBytes + kk * 32),
+                                bd, kIdesc, (ki | q | kk) != 0);
+                  }
+                }
+              }
+              mma_commit(&empty_bar[stage]);
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+              continue;
+            }
 #pragma unroll
             for (int q = 0; q < TAPS; ++q) {
               if (q < static_cast<int>(nq)) {
@@ -289,7 +326,44 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
         valid[mt] = tile_ok && rr < loaded_rows && r_w < a.box_w && ow < a.w_out && oh < a.h_out && img < a.n_img;
         obase[mt] = valid[mt] ? static_cast<int64_t>(img) * a.co * a.hw + static_cast<int64_t>(oh) * a.w_out + ow : 0;
       }
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * (MT * N);
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * (MT * kAccN);
+      if constexpr (TN2) {
+        // out[p] = D[p][co] + D[p+1][64 + co]: row p+1 is the next lane, or for lane 31 the first
+        // row of the next quarter, passed through smem (row 127 is never an output: qmax >= 1)
+        const int half = (warp - 4) / 4;
+        float* xb = xch + acc * (MT * 2 * 4 * 32);  // [mt][half][quarter][32 columns]
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int jj = 0; jj < N / 2; jj += 16) {
+            uint32_t e[16];
+            tmem_ld16(taddr + mt * kAccN + N + j_lo + jj, e);
+            if (lane == 0) {
+#pragma unroll
+              for (int q = 0; q < 16; ++q) xb[((mt * 2 + half) * 4 + quarter) * 32 + jj + q] = __uint_as_float(e[q]);
+            }
+          }
+        asm volatile("bar.sync 1, %0;\n" ::"r"(kEpiWarps * 32) : "memory");
+#pragma unroll
+        for (int jj = 0; jj < N / 2; jj += 16) {
+          const int j0 = j_lo + jj;
+          const uint32_t m0 = co_blk * N + j0;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            uint32_t d[16], e[16];
+            tmem_ld16(taddr + mt * kAccN + j0, d);
+            tmem_ld16(taddr + mt * kAccN + N + j0, e);
+            const float* nx = xb + ((mt * 2 + half) * 4 + (quarter + 1 < 4 ? quarter + 1 : quarter)) * 32 + jj;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              float en = __shfl_down_sync(0xffffffffu, __uint_as_float(e[q]), 1);
+              if (lane == 31) en = nx[q];
+              if (valid[mt] && m0 + q < a.co)
+                st_out(a.out + obase[mt] + static_cast<int64_t>(m0 + q) * a.hw, __uint_as_float(d[q]) + en);
+            }
+          }
+        }
+      } else
 #pragma unroll
       for (int jj = 0; jj < N / 2; jj += 16) {
         const int j0 = j_lo + jj;
@@ -381,7 +455,7 @@ inline double phase_tile(int64_t n, int64_t h_out, int64_t w_out, int64_t qmax, 
   return static_cast<double>(a.box_w) * a.rows * a.box_n / kTileM;
 }
 
-template <bool BF16, int N, int STAGES, int TAPS, int MT, bool PAIR = false>
+template <bool BF16, int N, int STAGES, int TAPS, int MT, bool PAIR = false, bool TN2 = false>
 static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64_t c_pad, int64_t h, int64_t w,
                         int64_t Mp, int64_t Kp, const NhwcFeed& feed, cudaStream_t stream, const char** err) {
   constexpr int kBK = BF16 ? 64 : 32;
@@ -426,7 +500,7 @@ static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64
   }
   a.co_tiles = static_cast<uint32_t>(Mp / N);
   const size_t smem = static_cast<size_t>(STAGES) * (MT * kPhRows + TAPS * (PAIR ? N / 2 : N)) * kRowBytes + 1024;
-  auto kern = conv_tc_phase_kernel<BF16, N, STAGES, TAPS, MT, PAIR>;
+  auto kern = conv_tc_phase_kernel<BF16, N, STAGES, TAPS, MT, PAIR, TN2>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
@@ -446,6 +520,8 @@ static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64
     grid = 2 * static_cast<uint32_t>(std::min<uint64_t>(items, static_cast<uint64_t>(clusters)));
     im2win_note_kernel(MT == 4 ? "conv_tc_phase_kernel (phase shift, CTA pair M=256, 4 tiles/CTA)"
                                : "conv_tc_phase_kernel (phase shift, CTA pair M=256, 2 tiles/CTA)");
+  } else if (TN2) {
+    im2win_note_kernel("conv_tc_phase_kernel (phase shift, tap pairs N=128, 2 tiles/item)");
   } else {
     im2win_note_kernel(MT == 4 ? "conv_tc_phase_kernel (phase shift, 4 tiles/item)"
                                : "conv_tc_phase_kernel (phase shift, 2 tiles/item)");
@@ -547,6 +623,16 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
   // without pairs (BF16 conv4 0.819 vs 0.811 ms, N=128); conv8 TF32 (N=128) 2% faster.
   const char* pair_env = getenv("IM2WIN_PAIR");
   const bool pair = pair_env && atoi(pair_env) > 0;
+  // tap pairs per MMA for Co <= 64 (2 pixel tiles per item).  Measured (tools/tn2_ab.py, conv
+  // alone): 4 taps per phase (conv4, 7x7 stride 2) BF16 817 -> 944 TF at N=128, 862 -> 953 at 512,
+  // 874 -> 881 at 2048; TF32 +11-26%; 3 taps (conv9, 3x3 stride 1) TF32 +3-6% but BF16 -8% (fewer
+  // taps to pair, half the filter reuse of 4 tiles per item).  IM2WIN_PHASE_TN2: 0 off, 1 auto, 2
+  // wherever legal.
+  const char* tn2_env = getenv("IM2WIN_PHASE_TN2");
+  const int tn2_mode = tn2_env ? atoi(tn2_env) : 1;
+  const bool tn2 = !pair && N == 64 && taps >= 2 && taps <= 4 &&
+                   (tn2_mode == 2 || (tn2_mode == 1 && (taps == 4 || (!bf16 && taps == 3))));
+  if (tn2) mt_sel = 2;
   a.pairs = (a.p_tiles + mt_sel * (pair ? 2 : 1) - 1) / (mt_sel * (pair ? 2 : 1));
   a.stride = static_cast<uint32_t>(stride);
   a.w_f = static_cast<uint32_t>(w_f);
@@ -561,6 +647,22 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
                                                              static_cast<int>(c_in), h_f, w_f, static_cast<int>(Mp),
                                                              static_cast<int>(Kc));
   int rc = 1;
+  if (tn2) {
+    // stage = 2 x 17 KB of A + taps x 8 KB of B (+ 4 KB static exchange buffer)
+#define IM2WIN_PHT(BF, ST, TP) \
+  rc = launch_phase<BF, 64, ST, TP, 2, false, true>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err)
+    if (bf16) {
+      if (taps == 2) IM2WIN_PHT(true, 4, 2);
+      else if (taps == 3) IM2WIN_PHT(true, 3, 3);
+      else IM2WIN_PHT(true, 3, 4);
+    } else {
+      if (taps == 2) IM2WIN_PHT(false, 4, 2);
+      else if (taps == 3) IM2WIN_PHT(false, 3, 3);
+      else IM2WIN_PHT(false, 3, 4);
+    }
+#undef IM2WIN_PHT
+    return rc == 0 ? 1 : -rc;
+  }
   // stage = 2 x 17 KB of A + taps x N x 128 B of B; as many stages as fit in 227 KB
 #define IM2WIN_PH(BF, NN, ST, TP)                                                                             \
   rc = pair ? launch_phase<BF, NN, ST, TP, 2, true>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err) \

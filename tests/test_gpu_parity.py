@@ -405,6 +405,52 @@ def test_tc_phase_kernel_edge_geometries(variant, monkeypatch):
         assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (n, c, h, w, co, hf, wf, s)
 
 
+@pytest.mark.parametrize("variant", ["tf32", "bf16"])
+def test_tc_phase_tap_pairs(variant, monkeypatch, layer_goldens):
+    """Tap pairs per MMA (IM2WIN_PHASE_TN2=2; B rows 64-127 = the next tap, D[p] + D[p+1] shifted
+    in the epilogue, odd last taps as N=64 MMAs): within tolerance on 2-4 taps per phase, stride 1
+    and 2, ragged widths and multi-row / multi-image tiles, on conv4 and conv9 with and without
+    the in-kernel feed, and close to the one-tap-per-MMA kernel."""
+    from paper_2306_14316_b200 import _lib
+
+    monkeypatch.setenv("IM2WIN_PHASE", "2")
+    cases = [(3, 64, 17, 19, 64, 7, 7, 2), (1, 64, 23, 9, 64, 3, 3, 2), (2, 32, 30, 31, 48, 5, 5, 2),
+             (5, 32, 8, 8, 64, 3, 3, 1), (2, 40, 12, 13, 64, 3, 3, 1), (1, 64, 140, 140, 64, 7, 7, 2),
+             (7, 64, 6, 7, 33, 3, 3, 1), (2, 64, 20, 21, 64, 7, 7, 1)]  # (last: 7 taps, no pairs)
+    for (n, c, h, w, co, hf, wf, s) in cases:
+        rng = np.random.default_rng(n * 100 + h + wf)
+        if (wf + s - 1) // s > 4:  # tap pairs cover 2-4 taps per phase: the plain kernel runs
+            monkeypatch.setenv("IM2WIN_PHASE_TN2", "2")
+            out = pkg.conv_im2win_opt(inp := rng.standard_normal((n, c, h, w), dtype=np.float32),
+                                      flt := rng.standard_normal((co, c, hf, wf), dtype=np.float32),
+                                      pkg.ConvParams(c, co, hf, wf, s), variant=variant, tc_path="fused").numpy()
+            assert "tap pairs" not in _lib.last_kernel()
+            assert pkg.normalized_max_diff(out, orc.conv_direct(inp, flt, s)) <= TC_TOL[variant]
+            continue
+        inp = rng.standard_normal((n, c, h, w), dtype=np.float32)
+        flt = rng.standard_normal((co, c, hf, wf), dtype=np.float32)
+        ref = orc.conv_direct(inp, flt, s)
+        params = pkg.ConvParams(c, co, hf, wf, s)
+        monkeypatch.setenv("IM2WIN_PHASE_TN2", "2")
+        out2 = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path="fused").numpy()
+        assert "tap pairs" in _lib.last_kernel(), (n, c, h, w, _lib.last_kernel())
+        monkeypatch.setenv("IM2WIN_PHASE_TN2", "0")
+        out0 = pkg.conv_im2win_opt(inp, flt, params, variant=variant, tc_path="fused").numpy()
+        assert pkg.normalized_max_diff(out2, ref) <= TC_TOL[variant], (n, c, h, w, co, hf, wf, s)
+        assert pkg.normalized_max_diff(out2, out0) <= TC_TOL[variant] / 2, (n, c, h, w, co, hf, wf, s)
+    monkeypatch.setenv("IM2WIN_PHASE_TN2", "2")
+    for name in ("conv4", "conv9"):
+        g = layer_goldens[name]
+        cfg = replace(BENCHMARKS[name], batch=g["batch"], seed=g["seed"])
+        inp, flt = make_inputs(cfg)
+        ref = orc.conv_direct(inp, flt, cfg.stride)
+        for feed in ("0", "2"):
+            monkeypatch.setenv("IM2WIN_FEED", feed)
+            out = pkg.conv_im2win_opt(inp, flt, cfg.params, variant=variant).numpy()
+            assert "tap pairs" in _lib.last_kernel(), (name, feed)
+            assert pkg.normalized_max_diff(out, ref) <= TC_TOL[variant], (name, feed)
+
+
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("shape", [(2, 3, 7, 9), (3, 64, 12, 12), (2, 96, 20, 20), (1, 130, 6, 10), (2, 40, 5, 5),
                                    (1, 256, 14, 14)])
