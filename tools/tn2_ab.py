@@ -1,6 +1,8 @@
 """Phase kernel, one tap per MMA (N=64, 4 tiles/item) vs tap pairs per MMA (N=128, 2 tiles/item):
 
-    python tools/tn2_ab.py [layers] [batch] [variants]
+    python tools/tn2_ab.py [layers] [batch] [variants] [switch]
+
+switch: IM2WIN_PHASE_TN2 (default; values 0/1) or IM2WIN_SHIFT_TN2 (values 0/2, the window-shift kernel).
 
 Conv alone on an existing channels-last copy (median of 7) and the one-call path; error =
 max|d| / rms(ref) against the FP32-exact call.  IM2WIN_PHASE_TN2 is read per launch.
@@ -21,6 +23,8 @@ from paper_2306_14316_b200.workloads import BENCHMARKS  # noqa: E402
 layers = (sys.argv[1] if len(sys.argv) > 1 else "conv4,conv9").split(",")
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 variants = (sys.argv[3] if len(sys.argv) > 3 else "bf16,tf32").split(",")
+switch = sys.argv[4] if len(sys.argv) > 4 else "IM2WIN_PHASE_TN2"
+on = "2" if switch == "IM2WIN_SHIFT_TN2" else "1"
 dev = torch.device("cuda:0")
 
 
@@ -53,8 +57,8 @@ for name in layers:
                          dtype=torch.bfloat16 if v == "bf16" else torch.float32)
         nhwc_into(x, xc)
         row = []
-        for mode in ("0", "1"):
-            os.environ["IM2WIN_PHASE_TN2"] = mode
+        for mode in ("0", on):
+            os.environ[switch] = mode
             out.fill_(float("nan"))
             t_conv = timed(lambda: conv_fused_into(xc, f, out, cfg.params, v))
             err = float((out - ref).abs().max() / rms)
@@ -62,5 +66,5 @@ for name in layers:
             t_one = timed(lambda: conv_fused_nchw_into(x, xc, f, out, cfg.params, v))
             row.append(f"TN2={mode}: conv {t_conv:7.3f} ms {cfg.flops / t_conv / 1e9:6.1f} TF, one-call "
                        f"{cfg.flops / t_one / 1e9:6.1f} TF, err {err:.1e} [{kern[22:]}]")
-        os.environ["IM2WIN_PHASE_TN2"] = "0"
+        os.environ[switch] = "0"
         print(f"{name:6s} {v:5s} N={batch} | " + " | ".join(row), flush=True)
