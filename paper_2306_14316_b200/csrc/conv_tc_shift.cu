@@ -36,11 +36,7 @@ IM2WIN_DEVICE uint64_t smem_desc_sw128_off(uint32_t addr) {
   return d;
 }
 
-// TN2: two filter columns per MMA (N' = 2N): the tiles of taps fw and fw+1 are adjacent in smem
-// (2N rows), both against the A tile shifted for fw; D columns N..2N-1 then hold tap fw+1 one
-// pixel early and the epilogue adds D[p][co] + D[p+1][N + co] (as in the phase kernel's tap
-// pairs); an odd last tap is a plain N-wide MMA into columns 0..N-1.
-template <bool BF16, int N, int STAGES, int WF, bool RB, bool TN2 = false>
+template <bool BF16, int N, int STAGES, int WF, bool RB>
 __global__ void __launch_bounds__(kTcThreadsFeed, 1)
     conv_tc_shift_kernel(const ShiftArgs a, const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b, const NhwcFeed feed) {
@@ -49,12 +45,9 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
   constexpr uint32_t kStageBytes = kABytes + kBBytes;
   constexpr int kBK = BF16 ? 64 : 32;
   constexpr int kUK = BF16 ? 16 : 8;
-  constexpr int kAccN = TN2 ? 2 * N : N;  // TMEM columns per tile
-  constexpr uint32_t kTmemCols = (2 * kAccN <= 128) ? 128 : (2 * kAccN <= 256 ? 256 : 512);
+  constexpr uint32_t kTmemCols = (2 * N <= 128) ? 128 : (2 * N <= 256 ? 256 : 512);
   constexpr uint32_t kIdesc = instr_desc<BF16, N>();
-  constexpr uint32_t kIdesc2 = instr_desc<BF16, (TN2 ? 2 * N : N)>();
   static_assert(kABytes % 1024 == 0, "A stage must keep 1024 B alignment");
-  static_assert(!TN2 || 2 * N <= 256, "tap pairs: UMMA N <= 256");
 
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[STAGES];
@@ -63,8 +56,6 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
   __shared__ __align__(8) uint64_t tempty_bar[2];
   __shared__ __align__(8) uint64_t bres_bar;
   __shared__ uint32_t tmem_base_sh;
-  // TN2: each quarter warp's first-row tap-(fw+1) columns, for the warp of the quarter before it
-  __shared__ float xch[TN2 ? 2 * 4 * N : 1];
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x / 32;
@@ -153,27 +144,12 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
       for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * kAccN;
+        const uint32_t tmem_d = tmem_base + acc * N;
         for (uint32_t ks = 0; ks < a.k_slabs; ++ks) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t abase = smem_u32(stages + stage * kStageBytes);
           const uint32_t bbase = RB ? smem_u32(smem) + ks * WF * N * kRowBytes : abase + kABytes;
-          if constexpr (TN2) {
-#pragma unroll
-            for (int fw = 0; fw < WF; fw += 2) {
-#pragma unroll
-              for (int kk = 0; kk < kBK / kUK; ++kk) {
-                const uint64_t ad = smem_desc_sw128(abase + fw * kRowBytes + kk * 32);
-                const uint64_t bd = smem_desc_sw128(bbase + fw * N * kRowBytes + kk * 32);
-                if (fw + 1 < WF) mma<BF16>(tmem_d, ad, bd, kIdesc2, (ks | fw | kk) != 0);
-                else mma<BF16>(tmem_d, ad, bd, kIdesc, (ks | fw | kk) != 0);
-              }
-            }
-            mma_commit(&empty_bar[stage]);
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
-            continue;
-          }
 #pragma unroll
           for (int fw = 0; fw < WF; ++fw) {
 #pragma unroll
@@ -214,39 +190,7 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
       const int64_t obase = valid ? static_cast<int64_t>(img) * a.co * a.hw + static_cast<int64_t>(oh) * a.w_out + ow : 0;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kAccN;
-      if constexpr (TN2) {
-        // out[p] = D[p][co] + D[p+1][N + co] (next lane; lane 31: the next quarter's first row via
-        // smem; row 127 is never an output since the pitch carries Wf - 1 >= 1 halo columns)
-        const int half = (warp - 4) / 4;
-        float* xb = xch + acc * (4 * N);  // [half][quarter][N/2 columns]
-#pragma unroll
-        for (int jj = 0; jj < N / 2; jj += 16) {
-          uint32_t e[16];
-          tmem_ld16(taddr + N + j_lo + jj, e);
-          if (lane == 0) {
-#pragma unroll
-            for (int q = 0; q < 16; ++q) xb[(half * 4 + quarter) * (N / 2) + jj + q] = __uint_as_float(e[q]);
-          }
-        }
-        asm volatile("bar.sync 1, %0;\n" ::"r"(kEpiWarps * 32) : "memory");
-        const float* nx = xb + (half * 4 + (quarter + 1 < 4 ? quarter + 1 : quarter)) * (N / 2);
-#pragma unroll
-        for (int jj = 0; jj < N / 2; jj += 16) {
-          const int j0 = j_lo + jj;
-          uint32_t d[16], e[16];
-          tmem_ld16(taddr + j0, d);
-          tmem_ld16(taddr + N + j0, e);
-          const uint32_t m0 = co_blk * N + j0;
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            float en = __shfl_down_sync(0xffffffffu, __uint_as_float(e[q]), 1);
-            if (lane == 31) en = nx[jj + q];
-            if (valid && m0 + q < a.co)
-              st_out(a.out + obase + static_cast<int64_t>(m0 + q) * a.hw, __uint_as_float(d[q]) + en);
-          }
-        }
-      } else
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * N;
 #pragma unroll
       for (int jj = 0; jj < N / 2; jj += 16) {
         const int j0 = j_lo + jj;
@@ -318,7 +262,7 @@ inline double shift_tile(int64_t n, int64_t h_out, int64_t w_out, int w_f, Shift
   return static_cast<double>(a.box_w) * a.rows * a.box_n / kTileM;
 }
 
-template <bool BF16, int N, int STAGES, int WF, bool RB, bool TN2 = false>
+template <bool BF16, int N, int STAGES, int WF, bool RB>
 static int launch_shift(ShiftArgs a, const void* x_cl, const void* packed, int64_t c_in, int64_t h, int64_t w,
                         int64_t Mp, int64_t Kp, const NhwcFeed& feed, cudaStream_t stream, const char** err) {
   constexpr int kBK = BF16 ? 64 : 32;
@@ -361,7 +305,7 @@ static int launch_shift(ShiftArgs a, const void* x_cl, const void* packed, int64
   const size_t smem = rb + static_cast<size_t>(STAGES) * (kARows + (RB ? 0 : WF * N)) * kRowBytes + 1024;
   // Measured on B200: the SW128 swizzle phase follows the absolute smem address, so the
   // row-shifted start address needs no descriptor base offset.
-  auto kern = conv_tc_shift_kernel<BF16, N, STAGES, WF, RB, TN2>;
+  auto kern = conv_tc_shift_kernel<BF16, N, STAGES, WF, RB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
@@ -372,12 +316,7 @@ static int launch_shift(ShiftArgs a, const void* x_cl, const void* packed, int64
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t tiles = static_cast<uint64_t>(a.n_tiles) * a.oh_tiles * a.ow_tiles * a.co_tiles;
   const uint32_t grid = tiles < static_cast<uint64_t>(sms) ? static_cast<uint32_t>(tiles) : static_cast<uint32_t>(sms);
-  if (TN2)
-    im2win_note_kernel(RB ? "conv_tc_shift_kernel (window shift, filter resident, tap pairs)"
-                          : "conv_tc_shift_kernel (window shift, tap pairs)");
-  else
-    im2win_note_kernel(RB ? "conv_tc_shift_kernel (window shift, filter resident)"
-                          : "conv_tc_shift_kernel (window shift)");
+  im2win_note_kernel(RB ? "conv_tc_shift_kernel (window shift, filter resident)" : "conv_tc_shift_kernel (window shift)");
   e = launch_tc_kernel(kern, grid, smem, stream, feed.src != nullptr, 1, a, map_a, map_b, feed_for(feed, grid, tiles));
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
@@ -446,25 +385,8 @@ int im2win_try_conv_tc_shift(const void* x_cl, const float* flt, float* out, voi
   // Filter-resident mode: when the packed filter fits next to 4 A stages it is loaded
   // once per CTA (one Co tile) and only window tiles stream through the ring.
   const size_t rb_bytes = static_cast<size_t>(a.k_slabs) * w_f * N * kRowBytes;
-  // tap pairs (IM2WIN_SHIFT_TN2: 0 off, 2 on; 3x3 filters): N' = 2N per MMA, + 2*4*N*4 B of static smem
-  const char* tn2_env = getenv("IM2WIN_SHIFT_TN2");
-  const bool tn2 = w_f == 3 && tn2_env && atoi(tn2_env) == 2;
-  const size_t xch_bytes = tn2 ? 2 * 4 * static_cast<size_t>(N) * 4 : 0;
-  const bool rb = Mp == N && rb_bytes + 4 * kARows * kRowBytes + 1024 + xch_bytes <= 227 * 1024 &&
+  const bool rb = Mp == N && rb_bytes + 4 * kARows * kRowBytes + 1024 <= 227 * 1024 &&
                   !(getenv("IM2WIN_SHIFT_RB") && atoi(getenv("IM2WIN_SHIFT_RB")) == 0);
-  if (tn2) {
-#define IM2WIN_SHT(BF, NN, ST, RBB) \
-  rc = launch_shift<BF, NN, ST, 3, RBB, true>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err)
-    if (bf16) {
-      if (N == 64) { if (rb) IM2WIN_SHT(true, 64, 4, true); else IM2WIN_SHT(true, 64, 5, false); }
-      else { if (rb) IM2WIN_SHT(true, 128, 4, true); else IM2WIN_SHT(true, 128, 3, false); }
-    } else {
-      if (N == 64) { if (rb) IM2WIN_SHT(false, 64, 4, true); else IM2WIN_SHT(false, 64, 5, false); }
-      else { if (rb) IM2WIN_SHT(false, 128, 4, true); else IM2WIN_SHT(false, 128, 3, false); }
-    }
-#undef IM2WIN_SHT
-    return rc == 0 ? 1 : -rc;
-  }
 #define IM2WIN_SH(BF, NN, ST, WFF, RBB) \
   rc = launch_shift<BF, NN, ST, WFF, RBB>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err)
   if (w_f == 3) {

@@ -2,7 +2,7 @@
 
     python tools/tn2_ab.py [layers] [batch] [variants] [switch]
 
-switch: IM2WIN_PHASE_TN2 (default; values 0/1) or IM2WIN_SHIFT_TN2 (values 0/2, the window-shift kernel).
+switch: IM2WIN_PHASE_TN2 (default; values 0/1).
 
 Conv alone on an existing channels-last copy (median of 7) and the one-call path; error =
 max|d| / rms(ref) against the FP32-exact call.  IM2WIN_PHASE_TN2 is read per launch.
