@@ -31,8 +31,8 @@ for (n, c, h, w, co, hf, wf, s, p) in cases:
                 continue
             pkg.conv_im2win_opt(x, f, params, variant=v, tc_path=path)
     pkg.conv_im2win_opt_host(x.cpu(), f.cpu(), params, chunk_images=1)
-# round 2: the in-kernel channels-last feed (forced on every TMA-fed kernel), CTA pairs, the
-# FP32 window-budget chunks
+# round 2: the in-kernel channels-last feed (forced on every TMA-fed kernel), CTA pairs, tap pairs
+# in the phase kernel (smem exchange between epilogue warps), the FP32 window-budget chunks
 import os  # noqa: E402
 
 for (n, c, h, w, co, hf, wf, s, p) in cases:
@@ -51,6 +51,19 @@ for (n, c, h, w, co, hf, wf, s, p) in cases:
     os.environ["IM2WIN_WINDOW_BUDGET"] = "1"
     pkg.conv_im2win_opt(torch.cat([x] * 5), f, params)
     del os.environ["IM2WIN_WINDOW_BUDGET"]
+# shapes the phase kernel takes (C >= 32, stride <= 2, Co <= 64): tap pairs with and without the feed
+for (n, c, h, w, co, hf, wf, s) in [(2, 64, 17, 19, 64, 7, 7, 2), (3, 32, 9, 10, 48, 3, 3, 1)]:
+    x = torch.from_numpy(rng.standard_normal((n, c, h, w), dtype=np.float32)).cuda()
+    f = torch.from_numpy(rng.standard_normal((co, c, hf, wf), dtype=np.float32)).cuda()
+    params = pkg.ConvParams(c, co, hf, wf, s)
+    for env in ({"IM2WIN_PHASE": "2", "IM2WIN_PHASE_TN2": "2"},
+                {"IM2WIN_FEED": "2", "IM2WIN_PHASE": "2", "IM2WIN_PHASE_TN2": "2"}):
+        os.environ.update(env)
+        for v in ("tf32", "bf16"):
+            pkg.conv_im2win_opt(x, f, params, variant=v, tc_path="fused")
+            assert "tap pairs" in pkg._lib.last_kernel(), pkg._lib.last_kernel()
+        for k in env:
+            del os.environ[k]
 # 4-byte-offset operands (the staged transform aligns its 16-byte copies to the address)
 for (n, c, h, w, co, hf, wf, s, p) in cases[:3]:
     base = torch.from_numpy(rng.standard_normal(1 + n * c * h * w, dtype=np.float32)).cuda()
