@@ -34,6 +34,7 @@ struct PhaseArgs {
   uint32_t box_w, pitch, rows, box_n;  // pixel tile: box_n images x rows output rows x box_w columns
   uint32_t ow_tiles, oh_tiles, n_tiles, p_tiles, pairs, co_tiles;
   uint32_t stride, w_f, c_slabs, k_iters;  // k_iters = Hf * stride * c_slabs
+  uint32_t k_total;                        // Kp of the packed filter (a box there is all zero fill)
 };
 
 constexpr int kPhRows = 136;  // 128 MMA rows + up to 8 rows of shift
@@ -54,16 +55,20 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
                          const NhwcFeed feed) {
   constexpr uint32_t kATile = kPhRows * kRowBytes;  // 17 KB, multiple of 1024
   constexpr uint32_t kABytes = MT * kATile;
-  constexpr int kBRows = PAIR ? N / 2 : N;           // filter rows staged by this CTA
+  // PAIR && TN2: a pair MMA is M=256 x N=128 -- CTA rank r holds tap 2j + r of pair j (all 64
+  // filter rows), so each CTA stages ceil(TAPS/2) tap tiles and B's halves are the two taps
+  constexpr bool kPT = PAIR && TN2;
+  constexpr int kBRows = PAIR && !TN2 ? N / 2 : N;  // filter rows per staged tile
+  constexpr int kBSlots = kPT ? (TAPS + 1) / 2 : TAPS;
   constexpr uint32_t kBTap = kBRows * kRowBytes;
-  constexpr uint32_t kStageBytes = kABytes + TAPS * kBTap;
+  constexpr uint32_t kStageBytes = kABytes + kBSlots * kBTap;
   constexpr int kBK = BF16 ? 64 : 32;
   constexpr int kUK = BF16 ? 16 : 8;
   constexpr int kAccN = TN2 ? 2 * N : N;  // TMEM columns per pixel tile
   constexpr uint32_t kTmemCols = (2 * MT * kAccN <= 128) ? 128 : (2 * MT * kAccN <= 256 ? 256 : 512);
   constexpr uint32_t kIdesc = instr_desc_m<BF16, N, PAIR ? 256 : 128>();
-  constexpr uint32_t kIdesc2 = instr_desc_m<BF16, 2 * N, 128>();
-  static_assert(!TN2 || (!PAIR && N == 64), "tap pairs: single CTA, Co tile 64");
+  constexpr uint32_t kIdesc2 = instr_desc_m<BF16, 2 * N, PAIR ? 256 : 128>();
+  static_assert(!TN2 || N == 64, "tap pairs: Co tile 64");
   constexpr uint32_t kCtas = PAIR ? 2 : 1;
   static_assert(kATile % 1024 == 0 && kBTap % 1024 == 0, "tiles must keep 1024 B alignment");
   static_assert(2 * MT * kAccN <= 512, "TMEM holds 512 fp32 columns");
@@ -153,7 +158,30 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * kStageBytes;
           const CUtensorMap* am = r == 0 ? &tmap_a0 : &tmap_a1;
-          if constexpr (PAIR) {
+          if constexpr (kPT) {
+            // pair j: this CTA stages tap 2j + rank (a tap past the phase's last is a box beyond the
+            // packed filter's K extent: zero-filled, so its half of the MMA adds nothing)
+            const uint32_t slots = (nq + 1) / 2;
+            if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (MT * a_box_bytes + slots * kBTap));
+            const uint32_t fb = mapa_shared(&full_bar[stage], 0);
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              asm volatile(
+                  "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+                  "[%1, {%3, %4, %5, %6, %7}], [%2];\n" ::"r"(smem_u32(st + mt * kATile)),
+                  "l"(am), "r"(fb), "r"(c0), "r"(ow0[mt]), "r"(fh % s), "r"(oh0[mt] + fh / s), "r"(n0[mt])
+                  : "memory");
+            }
+            for (uint32_t j = 0; j < slots; ++j) {
+              const uint32_t q = 2 * j + rank;
+              const uint32_t kx = q < nq ? (fh * a.w_f + s * q + r) * a.c_slabs * kBK + c0 : a.k_total;
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+                  "[%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(st + kABytes + j * kBTap)),
+                  "l"(&tmap_b), "r"(fb), "r"(kx), "r"(co_blk * N)
+                  : "memory");
+            }
+          } else if constexpr (PAIR) {
             // both CTAs' loads complete on rank 0's full barrier, which expects the bytes of both
             if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (MT * a_box_bytes + nq * kBTap));
             const uint32_t fb = mapa_shared(&full_bar[stage], 0);
@@ -265,7 +293,7 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
       for (uint32_t t = PAIR ? blockIdx.x / 2 : blockIdx.x; t < total; t += PAIR ? gridDim.x / 2 : gridDim.x) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * (MT * N);
+        const uint32_t tmem_d = tmem_base + acc * (MT * kAccN);
         for (uint32_t ki = 0; ki < a.k_iters; ++ki) {
           const uint32_t r = (ki / a.c_slabs) % s;
           const uint32_t nq = (a.w_f - r + s - 1) / s;
@@ -273,6 +301,25 @@ __global__ void __launch_bounds__(kTcThreadsFeed, 1)
           tc_fence_after();
           const uint32_t abase = smem_u32(smem + stage * kStageBytes);
           const uint32_t bbase = abase + kABytes;
+          if constexpr (kPT) {
+#pragma unroll
+            for (int j = 0; j < kBSlots; ++j) {
+              if (2 * j < static_cast<int>(nq)) {
+#pragma unroll
+                for (int kk = 0; kk < kBK / kUK; ++kk) {
+                  const uint64_t bd = smem_desc_sw128(bbase + j * kBTap + kk * 32);
+#pragma unroll
+                  for (int mt = 0; mt < MT; ++mt)
+                    mma_pair<BF16>(tmem_d + mt * kAccN,
+                                   smem_desc_sw128(abase + mt * kATile + 2 * j * kRowBytes + kk * 32), bd, kIdesc2,
+                                   (ki | j | kk) != 0);
+                }
+              }
+            }
+            mma_commit_pair(&empty_bar[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
 #pragma unroll
           for (int q = 0; q < TAPS; ++q) {
             if (q < static_cast<int>(nq)) {
@@ -488,7 +535,7 @@ static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64
   {
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(Mp)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(Kp) * esz};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(PAIR ? N / 2 : N)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(PAIR && !TN2 ? N / 2 : N)};
     cuuint32_t estr[2] = {1, 1};
     CUresult res = enc(&map_b, dt, 2, const_cast<void*>(packed), dims, strides, box, estr,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -499,7 +546,9 @@ static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64
     }
   }
   a.co_tiles = static_cast<uint32_t>(Mp / N);
-  const size_t smem = static_cast<size_t>(STAGES) * (MT * kPhRows + TAPS * (PAIR ? N / 2 : N)) * kRowBytes + 1024;
+  const int b_rows = PAIR && TN2 ? (TAPS + 1) / 2 * N : TAPS * (PAIR ? N / 2 : N);  // staged filter rows
+  const size_t smem = static_cast<size_t>(STAGES) * (MT * kPhRows + b_rows) * kRowBytes + 1024;
+  a.k_total = static_cast<uint32_t>(Kp);
   auto kern = conv_tc_phase_kernel<BF16, N, STAGES, TAPS, MT, PAIR, TN2>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) {
@@ -518,8 +567,9 @@ static int launch_phase(PhaseArgs a, const void* x_cl, const void* packed, int64
       return 2;
     }
     grid = 2 * static_cast<uint32_t>(std::min<uint64_t>(items, static_cast<uint64_t>(clusters)));
-    im2win_note_kernel(MT == 4 ? "conv_tc_phase_kernel (phase shift, CTA pair M=256, 4 tiles/CTA)"
-                               : "conv_tc_phase_kernel (phase shift, CTA pair M=256, 2 tiles/CTA)");
+    im2win_note_kernel(TN2 ? "conv_tc_phase_kernel (phase shift, CTA pair M=256 x tap pairs N=128, 2 tiles/CTA)"
+                       : MT == 4 ? "conv_tc_phase_kernel (phase shift, CTA pair M=256, 4 tiles/CTA)"
+                                 : "conv_tc_phase_kernel (phase shift, CTA pair M=256, 2 tiles/CTA)");
   } else if (TN2) {
     im2win_note_kernel("conv_tc_phase_kernel (phase shift, tap pairs N=128, 2 tiles/item)");
   } else {
@@ -630,7 +680,7 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
   // wherever legal.
   const char* tn2_env = getenv("IM2WIN_PHASE_TN2");
   const int tn2_mode = tn2_env ? atoi(tn2_env) : 1;
-  const bool tn2 = !pair && N == 64 && taps >= 2 && taps <= 4 &&
+  const bool tn2 = N == 64 && taps >= 2 && taps <= 4 &&
                    (tn2_mode == 2 || (tn2_mode == 1 && (taps == 4 || (!bf16 && taps == 3))));
   if (tn2) mt_sel = 2;
   a.pairs = (a.p_tiles + mt_sel * (pair ? 2 : 1) - 1) / (mt_sel * (pair ? 2 : 1));
@@ -649,8 +699,9 @@ int im2win_try_conv_tc_phase(const void* x_cl, const float* flt, float* out, voi
   int rc = 1;
   if (tn2) {
     // stage = 2 x 17 KB of A + taps x 8 KB of B (+ 4 KB static exchange buffer)
-#define IM2WIN_PHT(BF, ST, TP) \
-  rc = launch_phase<BF, 64, ST, TP, 2, false, true>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err)
+#define IM2WIN_PHT(BF, ST, TP)                                                                               \
+  rc = pair ? launch_phase<BF, 64, 4, TP, 2, true, true>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err) \
+            : launch_phase<BF, 64, ST, TP, 2, false, true>(a, x_cl, workspace, c_pad, h, w, Mp, Kp, feed, stream, err)
     if (bf16) {
       if (taps == 2) IM2WIN_PHT(true, 4, 2);
       else if (taps == 3) IM2WIN_PHT(true, 3, 3);

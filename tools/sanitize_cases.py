@@ -57,7 +57,8 @@ for (n, c, h, w, co, hf, wf, s) in [(2, 64, 17, 19, 64, 7, 7, 2), (3, 32, 9, 10,
     f = torch.from_numpy(rng.standard_normal((co, c, hf, wf), dtype=np.float32)).cuda()
     params = pkg.ConvParams(c, co, hf, wf, s)
     for env in ({"IM2WIN_PHASE": "2", "IM2WIN_PHASE_TN2": "2"},
-                {"IM2WIN_FEED": "2", "IM2WIN_PHASE": "2", "IM2WIN_PHASE_TN2": "2"}):
+                {"IM2WIN_FEED": "2", "IM2WIN_PHASE": "2", "IM2WIN_PHASE_TN2": "2"},
+                {"IM2WIN_PAIR": "1", "IM2WIN_PHASE": "2", "IM2WIN_PHASE_TN2": "2"}):
         os.environ.update(env)
         for v in ("tf32", "bf16"):
             pkg.conv_im2win_opt(x, f, params, variant=v, tc_path="fused")
