@@ -482,9 +482,9 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
   {
     cuuint64_t dims[5] = {static_cast<cuuint64_t>(w_f) * c_in, static_cast<cuuint64_t>(h_f), a.w_out, a.h_out,
                           a.n_img};
-    const cuuint64_t vs = tc_v_stride() > 0 ? static_cast<cuuint64_t>(tc_v_stride()) : static_cast<cuuint64_t>(stride);
     cuuint64_t strides[4] = {static_cast<cuuint64_t>(w) * c_in * esz, static_cast<cuuint64_t>(stride) * c_in * esz,
-                             vs * w * c_in * esz, static_cast<cuuint64_t>(h) * w * c_in * esz};
+                             static_cast<cuuint64_t>(stride) * w * c_in * esz,
+                             static_cast<cuuint64_t>(h) * w * c_in * esz};
     cuuint32_t box[5] = {static_cast<cuuint32_t>(kBK), 1, a.box_w, a.box_h, a.box_n};
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     CUresult r = enc(&map_a, dt, 5, const_cast<void*>(x_cl), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -552,102 +552,6 @@ static int launch_fused(FusedArgs a, const void* x_cl, const void* packed, int64
 int64_t im2win_nhwc_channel_pitch(int64_t c, int bf16) {
   const int64_t q = bf16 ? 8 : 4;
   return (c + q - 1) / q * q;
-}
-
-namespace im2win {
-namespace tc {
-// Row-stacked channels-last copy for few-channel inputs: pixel (img, oh, w) holds the Hf input
-// rows a window of output row oh covers, as channels cc = c*Hf + fh:
-//   S[img][oh][w][c*Hf + fh] = X[img][c][oh*s + fh][w]   (pitch kp, zero padded).
-// The layer is then a 1 x Wf conv with horizontal stride s over an Ho-row image of C*Hf channels
-// (filter [Co][C][Hf][Wf] == [Co][C*Hf][1][Wf]): a window is Wf consecutive pixels of C*Hf
-// channels -- conv3 (7x7, C=3): 3 box rows of 128 B per output pixel instead of 7.
-template <bool BF16>
-__global__ void __launch_bounds__(256) nchw_to_stacked_kernel(const float* __restrict__ src, void* __restrict__ dst,
-                                                              uint32_t c_in, uint32_t h, uint32_t w, uint32_t h_f,
-                                                              uint32_t stride, uint32_t h_out, uint32_t kp,
-                                                              uint64_t pixels) {
-  constexpr uint32_t G = BF16 ? 8 : 4;  // k per 16-byte chunk
-  __shared__ uint4 stage[8][32 * 8];    // per warp: 32 pixel rows of <= 8 chunks (128 B)
-  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t kreal = c_in * h_f, chunks = kp / G;
-  uint4* out = reinterpret_cast<uint4*>(dst);
-  for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * 8 + warp) * 32; base < pixels;
-       base += static_cast<uint64_t>(gridDim.x) * 8 * 32) {
-    const uint64_t px = base + lane;
-    if (px < pixels) {
-      const uint32_t x = static_cast<uint32_t>(px % w);
-      const uint64_t r = px / w;
-      const uint32_t oh = static_cast<uint32_t>(r % h_out);
-      const uint64_t img = r / h_out;
-      const float* s0 = src + img * c_in * h * w + static_cast<uint64_t>(oh * stride) * w + x;
-      uint32_t c = 0, fh = 0;
-      for (uint32_t q = 0; q < chunks; ++q) {
-        float v[G];
-#pragma unroll
-        for (uint32_t j = 0; j < G; ++j) {
-          v[j] = (q * G + j < kreal) ? __ldg(s0 + (static_cast<uint64_t>(c) * h + fh) * w) : 0.0f;
-          if (++fh == h_f) {
-            fh = 0;
-            ++c;
-          }
-        }
-        uint4 u;
-        if constexpr (BF16) {
-          u.x = pack_bf16x2(v[0], v[1]);
-          u.y = pack_bf16x2(v[2], v[3]);
-          u.z = pack_bf16x2(v[4], v[5]);
-          u.w = pack_bf16x2(v[6], v[7]);
-        } else {
-          u = make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
-        }
-        stage[warp][lane * chunks + q] = u;
-      }
-    }
-    __syncwarp();
-    // the warp's 32 pixel rows are contiguous in the copy: coalesced 16-byte stores
-    const uint32_t n_valid = pixels - base < 32 ? static_cast<uint32_t>(pixels - base) : 32u;
-    for (uint32_t i = lane; i < n_valid * chunks; i += 32) out[base * chunks + i] = stage[warp][i];
-    __syncwarp();
-  }
-}
-}  // namespace tc
-}  // namespace im2win
-
-// Whether the one-call path uses the row-stacked copy (IM2WIN_STACK: 0 never, 1 auto, 2 always).
-static bool stacked_applies(int64_t c_in, int h_f) {
-  const char* e = getenv("IM2WIN_STACK");
-  const int mode = e ? atoi(e) : 0;
-  const int64_t kp = c_in * h_f;  // stacked channels: rows of <= 128 bytes (bf16 64, tf32 32)
-  return kp <= 32 && ((mode == 2 && h_f > 1) || (mode == 1 && c_in <= 4 && h_f >= 5));
-}
-
-static int launch_nchw_to_stacked(const float* src, void* dst, int64_t n, int64_t c_in, int64_t h, int64_t w, int h_f,
-                                  int stride, int bf16, cudaStream_t stream, const char** err) {
-  const int64_t h_out = (h - h_f) / stride + 1;
-  const int64_t kp = im2win_nhwc_channel_pitch(c_in * h_f, bf16);
-  if (kp * (bf16 ? 2 : 4) > 128) {
-    *err = "nchw_to_stacked: stacked rows over 128 bytes";
-    return 1;
-  }
-  const uint64_t pixels = static_cast<uint64_t>(n * h_out * w);
-  const uint32_t g = static_cast<uint32_t>(std::min<uint64_t>((pixels + 255) / 256, 148 * 16));
-  if (bf16)
-    im2win::tc::nchw_to_stacked_kernel<true><<<g, 256, 0, stream>>>(
-        src, dst, static_cast<uint32_t>(c_in), static_cast<uint32_t>(h), static_cast<uint32_t>(w),
-        static_cast<uint32_t>(h_f), static_cast<uint32_t>(stride), static_cast<uint32_t>(h_out),
-        static_cast<uint32_t>(kp), pixels);
-  else
-    im2win::tc::nchw_to_stacked_kernel<false><<<g, 256, 0, stream>>>(
-        src, dst, static_cast<uint32_t>(c_in), static_cast<uint32_t>(h), static_cast<uint32_t>(w),
-        static_cast<uint32_t>(h_f), static_cast<uint32_t>(stride), static_cast<uint32_t>(h_out),
-        static_cast<uint32_t>(kp), pixels);
-  const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    *err = cudaGetErrorString(e);
-    return 2;
-  }
-  return 0;
 }
 
 namespace im2win {
@@ -820,17 +724,6 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
   // feed_src != nullptr: x_cl is scratch, produced from the NCHW input inside the conv kernel
   // (counters at the end of the workspace, see im2win_tc_feed_counters)
   NhwcFeed feed{};
-  if (feed_src && stacked_applies(c_in, h_f)) {
-    const int rc = launch_nchw_to_stacked(feed_src, const_cast<void*>(x_cl), n, c_in, h, w, h_f, stride, bf16, stream,
-                                          err);
-    if (rc) return rc;
-    const int64_t h_o = (h - h_f) / stride + 1;
-    tc_v_stride() = 1;
-    const int rc2 = im2win_launch_conv_tc_fused(x_cl, flt, out, workspace, n, c_in * h_f, h_o, w, c_out, 1, w_f,
-                                                stride, bf16, nullptr, stream, err);
-    tc_v_stride() = 0;
-    return rc2;
-  }
   if (feed_src) {
     // In-kernel feed or a copy kernel first.  Measured (tools/feed_ab.py): the feed warps share the
     // SM's L1/shared-memory datapath and HBM with the conv, so overlap pays only where the conv's
@@ -876,8 +769,7 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
     }
   }
   const int64_t cp = im2win_nhwc_channel_pitch(c_in, bf16);  // channel pitch of x_cl
-  const bool stacked = tc_v_stride() > 0;  // row-stacked input: rows already strided
-  const int64_t h_out = (h - h_f) / (stacked ? tc_v_stride() : stride) + 1, w_out = (w - w_f) / stride + 1;
+  const int64_t h_out = (h - h_f) / stride + 1, w_out = (w - w_f) / stride + 1;
   int N = c_out <= 64 ? 64 : c_out <= 96 ? 96 : c_out <= 128 ? 128 : 256;
   const int bk = bf16 ? 64 : 32;
   const int64_t Kfh = (w_f * cp + bk - 1) / bk * bk;
@@ -932,14 +824,14 @@ int im2win_launch_conv_tc_fused(const void* x_cl, const float* flt, float* out, 
   {
     // the phase kernel reuses each loaded A tile for every tap of a stride phase (any stride <= 2)
     const double util = static_cast<double>(a.box_w) * a.box_h * a.box_n / kTileM;
-    const int rc = stacked ? 0 : im2win_try_conv_tc_phase(x_cl, flt, out, workspace, n, c_in, cp, h, w, c_out, h_f, w_f, stride,
+    const int rc = im2win_try_conv_tc_phase(x_cl, flt, out, workspace, n, c_in, cp, h, w, c_out, h_f, w_f, stride,
                                             bf16, util, feed, stream, err);
     if (rc != 0) return rc > 0 ? 0 : -rc;
   }
   {
     // stride-1 layers: the window-shift kernel reuses each loaded A tile for all Wf taps
     const double util = static_cast<double>(a.box_w) * a.box_h * a.box_n / kTileM;
-    const int rc = stacked ? 0 : im2win_try_conv_tc_shift(x_cl, flt, out, workspace, n, c_in, cp, h, w, c_out, h_f, w_f, stride,
+    const int rc = im2win_try_conv_tc_shift(x_cl, flt, out, workspace, n, c_in, cp, h, w, c_out, h_f, w_f, stride,
                                             bf16, util, feed, stream, err);
     if (rc != 0) return rc > 0 ? 0 : -rc;
   }

@@ -472,13 +472,6 @@ inline NhwcFeed feed_for(const NhwcFeed& f, uint64_t grid, uint64_t items) {
 // Launch of a TMA-fed conv kernel: with a feed, the extra converter warps and a cooperative
 // launch (the CTAs wait on each other's feed units, so all must be co-resident).
 // cluster = 2: CTA pairs (cta_group::2 kernels).
-// Vertical stride of the fused kernel's window boxes when it differs from the horizontal one
-// (the row-stacked copy of few-channel inputs has its rows already strided: 1); 0 = same.
-inline int& tc_v_stride() {
-  static thread_local int v = 0;
-  return v;
-}
-
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_tc_kernel(void (*kern)(KArgs...), uint32_t grid, size_t smem, cudaStream_t stream,
                                     bool feed, int cluster, Args&&... args) {
