@@ -1,8 +1,8 @@
 """Phase kernel, one tap per MMA (N=64, 4 tiles/item) vs tap pairs per MMA (N=128, 2 tiles/item):
 
-    python tools/tn2_ab.py [layers] [batch] [variants] [switch]
+    python tools/tn2_ab.py [layers] [batch] [variants] [switch] [on-value]
 
-switch: IM2WIN_PHASE_TN2 (default; values 0/1).
+switch: IM2WIN_PHASE_TN2 (default), compared at 0 and the value given last (1 auto, 2 forced).
 
 Conv alone on an existing channels-last copy (median of 7) and the one-call path; error =
 max|d| / rms(ref) against the FP32-exact call.  IM2WIN_PHASE_TN2 is read per launch.
@@ -24,7 +24,7 @@ layers = (sys.argv[1] if len(sys.argv) > 1 else "conv4,conv9").split(",")
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 variants = (sys.argv[3] if len(sys.argv) > 3 else "bf16,tf32").split(",")
 switch = sys.argv[4] if len(sys.argv) > 4 else "IM2WIN_PHASE_TN2"
-on = "2" if switch == "IM2WIN_SHIFT_TN2" else "1"
+on = sys.argv[5] if len(sys.argv) > 5 else "1"  # "2": tap pairs wherever legal
 dev = torch.device("cuda:0")
 
 
