@@ -361,20 +361,23 @@ def tensor_peaks(dev, stream) -> dict:
 
 
 def fp32_peaks(lib, dev, stream) -> dict:
-    """FP32 CUDA-core peaks measured in this run: FMUL+FADD (bit-exact variant) and FFMA chains."""
+    """FP32 CUDA-core peaks measured in this run: the bit-exact multiply-then-add as scalar FMUL+FADD
+    and in the packed FFMA2 form the conv kernel issues (`exact` = the higher of the two: the ceiling
+    of a bit-exact conv), and FFMA chains."""
     import torch
 
     sink = torch.empty(256, device=dev)
     peak = {}
-    for exact in (1, 0):
+    for mode, key, chains in ((1, "exact_scalar", 32), (2, "exact_packed", 64), (0, "ffma", 32)):
         iters, blocks = 1 << 15, 148 * 8
-        lib.im2win_bench_fp32_peak(sink.data_ptr(), exact, 256, blocks, stream.cuda_stream)
+        lib.im2win_bench_fp32_peak(sink.data_ptr(), mode, 256, blocks, stream.cuda_stream)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        lib.im2win_bench_fp32_peak(sink.data_ptr(), exact, iters, blocks, stream.cuda_stream)
+        lib.im2win_bench_fp32_peak(sink.data_ptr(), mode, iters, blocks, stream.cuda_stream)
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        peak["exact" if exact else "ffma"] = 2 * 32 * iters * 256 * blocks / (e0.elapsed_time(e1) * 1e-3) / 1e12
+        peak[key] = 2 * chains * iters * 256 * blocks / (e0.elapsed_time(e1) * 1e-3) / 1e12
+    peak["exact"] = max(peak["exact_scalar"], peak["exact_packed"])
     return peak
 
 
@@ -707,7 +710,8 @@ def main() -> None:
                                     " (FP32: im2win windows gathered straight from NCHW, no Ĩ pass)"
                                     if windows_path is not None else "")},
               "windows_path": windows_path,
-              "peaks": {"fp32_exact_tflops": fp["exact"], "fp32_ffma_tflops": fp["ffma"],
+              "peaks": {"fp32_exact_tflops": fp["exact"], "fp32_exact_scalar_tflops": fp["exact_scalar"],
+                        "fp32_exact_packed_tflops": fp["exact_packed"], "fp32_ffma_tflops": fp["ffma"],
                         "hbm_gbs": peaks["hbm_gbs"], "bf16_tflops_file": peaks.get("bf16_tflops"),
                         "source": peaks["source"] + "; fp32 probes measured in this run"}}
 
@@ -821,15 +825,16 @@ def main() -> None:
                 "traffic": None}
     else:
         pk = fp["exact"] if args.variant == "fp32-exact" else fp["ffma"]
-        roof = {"bound": "fp32-simt", "kernel": "conv_simt_kernel " + ("FMUL+FADD" if args.variant == "fp32-exact"
-                                                                        else "FFMA")
+        roof = {"bound": "fp32-simt", "kernel": "conv_simt_kernel " + ("exact mul-then-add, packed FFMA2 pairs"
+                                                                        if args.variant == "fp32-exact" else "FFMA")
                 + (", windows gathered from NCHW" if fp32_nchw else ""),
                 "achieved": flops_step / (conv_ms_total * 1e-3) / 1e12, "peak": pk, "unit": "TFLOP/s",
                 "traffic": traffic and traffic["conv_bytes_per_launch"]}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["conv_share"] = conv_ms_total / (conv_ms_total + tr_ms_total)
     detail["roofline"] = dict(roof, traffic_detail=traffic,
-                              peak_source="FP32: im2win_bench_fp32_peak in this run (148x8 CTAs of independent chains)",
+                              peak_source="FP32: im2win_bench_fp32_peak in this run (148x8 CTAs of independent "
+                                          "chains; exact = max of scalar FMUL+FADD and the packed FFMA2 pair form)",
                               achieved_note="sum of the step's conv FLOPs / sum of the conv calls' mean durations "
                                             "(CUDA events inside the timed region)")
     cpu_short = None

@@ -74,6 +74,7 @@ struct ConvArgs {
   uint32_t m_tiles;
   uint32_t vec_out;                 // Ho*Wo % 4 == 0: 16-byte output stores
   uint32_t n_base;                  // first GEMM column of this launch (tail launches)
+  float neg_zero, one;              // -0.0f and 1.0f, opaque to the compiler (packed exact MACs)
 };
 
 // ---------------------------------------------------------------------------
@@ -111,6 +112,40 @@ IM2WIN_DEVICE float mac(float acc, float a, float b) {
   }
 }
 
+#ifndef IM2WIN_SIMT_FP2
+#define IM2WIN_SIMT_FP2 1  // exact multiply-then-add as two packed FFMA2 (0: scalar FMUL + FADD)
+#endif
+
+// One micro-tile row: acc[j] = rn(acc[j] + rn(a * fb[j])), ascending k per element (the caller's
+// k loop).  IM2WIN_SIMT_FP2: the same two roundings per element through the packed sm_100
+// FMUL2/FADD2 (per component identical to __fmul_rn/__fadd_rn): half the FP instructions.
+template <bool EXACT, int MT, bool FP2 = IM2WIN_SIMT_FP2>
+IM2WIN_DEVICE void mac_row(float (&acc)[MT], float a, const float (&fb)[MT], float nz, float one) {
+#if IM2WIN_SIMT_FP2
+  if constexpr (EXACT && FP2) {
+    // rn(a*b) = fma(a, b, -0) and rn(c + p) = fma(c, 1, p) exactly (signed zeros included); -0
+    // and 1 arrive as kernel arguments so ptxas cannot see through them and contract the pair
+    // into one FFMA2 (it fuses mul.rn.f32x2 + add.rn.f32x2 and the __fmul2_rn/__fadd2_rn pair)
+#pragma unroll
+    for (int j = 0; j < MT; j += 2) {
+      uint64_t p, c;
+      asm("{\n\t.reg .b64 aa, bb, zz;\n\tmov.b64 aa, {%1, %1};\n\tmov.b64 bb, {%2, %3};\n\t"
+          "mov.b64 zz, {%4, %4};\n\tfma.rn.f32x2 %0, aa, bb, zz;\n\t}\n"
+          : "=l"(p) : "f"(a), "f"(fb[j]), "f"(fb[j + 1]), "f"(nz));
+      asm("{\n\t.reg .b64 cc, oo;\n\tmov.b64 cc, {%1, %2};\n\tmov.b64 oo, {%4, %4};\n\t"
+          "fma.rn.f32x2 %0, cc, oo, %3;\n\t}\n"
+          : "=l"(c) : "f"(acc[j]), "f"(acc[j + 1]), "l"(p), "f"(one));
+      asm("mov.b64 {%0, %1}, %2;\n" : "=f"(acc[j]), "=f"(acc[j + 1]) : "l"(c));
+    }
+    return;
+  }
+#endif
+  (void)nz;
+  (void)one;
+#pragma unroll
+  for (int j = 0; j < MT; ++j) acc[j] = mac<EXACT>(acc[j], a, fb[j]);
+}
+
 // MT: register micro-tile MT x MT per thread (8: two 4x4 quadrants, the paper's
 // 8x8; 4: one 4x4 quadrant, for layers too small to fill 148 SMs with 8x8 threads).
 // SD: the per-k offset table delta[] is staged in shared memory once per CTA
@@ -128,6 +163,8 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? ((BM / MT) * 
   constexpr int HALVES = MT / 4;              // 4-wide quadrants per axis
   constexpr int PR = IM2WIN_SIMT_PART_ROWS;   // window rows per gather part
   constexpr int PARTS = BK / PR;              // gather parts per slab
+  // packed exact MACs everywhere but the 96-row tile (conv1/conv2: 3-5% slower with them)
+  constexpr bool kFP2 = IM2WIN_SIMT_FP2 && BM != 96;
   static_assert(PR % 4 == 0 && BK % PR == 0, "parts are whole int4 delta loads");
   static_assert(MT == 4 || MT == 8, "micro-tile is 4x4 or 8x8");
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -276,9 +313,7 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? ((BM / MT) * 
           }
       }
 #pragma unroll
-      for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int j = 0; j < MT; ++j) acc[i][j] = mac<EXACT>(acc[i][j], fa[i], fb[j]);
+      for (int i = 0; i < MT; ++i) mac_row<EXACT, MT, kFP2>(acc[i], fa[i], fb, a.neg_zero, a.one);
     }
   };
   auto no_hook = [](int) {};
@@ -348,9 +383,7 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? ((BM / MT) * 
           fb[4 * h] = bv.x; fb[4 * h + 1] = bv.y; fb[4 * h + 2] = bv.z; fb[4 * h + 3] = bv.w;
         }
 #pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-          for (int j = 0; j < MT; ++j) acc[i][j] = mac<EXACT>(acc[i][j], fa[i], fb[j]);
+        for (int i = 0; i < MT; ++i) mac_row<EXACT, MT, kFP2>(acc[i], fa[i], fb, a.neg_zero, a.one);
       }
     }
   }
@@ -469,9 +502,7 @@ __global__ void __launch_bounds__(256, 2) conv_simt_smallk_kernel(const ConvArgs
           fb[4 * h] = bv.x; fb[4 * h + 1] = bv.y; fb[4 * h + 2] = bv.z; fb[4 * h + 3] = bv.w;
         }
 #pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-          for (int j = 0; j < MT; ++j) acc[i][j] = mac<EXACT>(acc[i][j], fa[i], fb[j]);
+        for (int i = 0; i < MT; ++i) mac_row<EXACT, MT>(acc[i], fa[i], fb, a.neg_zero, a.one);
       }
     }
     __syncthreads();  // buffer b is free for the gather of tile it + 2
@@ -662,6 +693,8 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
   a.fd_hw = FastDiv(static_cast<uint32_t>(hw));
   a.fd_wo = FastDiv(static_cast<uint32_t>(w_out));
   a.vec_out = (hw % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0) ? 1u : 0u;
+  a.neg_zero = -0.0f;
+  a.one = 1.0f;
 
   cudaError_t e = cudaSuccess;
 #ifndef IM2WIN_SIMT_STAGES
