@@ -74,6 +74,8 @@ struct ConvArgs {
   uint32_t m_tiles;
   uint32_t vec_out;                 // Ho*Wo % 4 == 0: 16-byte output stores
   uint32_t n_base;                  // first GEMM column of this launch (tail launches)
+  uint32_t m_base;                  // first output channel of this launch (row-split launches)
+  uint32_t co_out;                  // output channels (image stride / hw); M may stop short of it
   float neg_zero, one;              // -0.0f and 1.0f, opaque to the compiler (packed exact MACs)
 };
 
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? ((BM / MT) * 
   const int tid = threadIdx.x;
   const uint32_t m_tile = blockIdx.x % a.m_tiles;
   const uint32_t n_tile = blockIdx.x / a.m_tiles;
-  const int m0 = m_tile * BM;
+  const int m0 = a.m_base + m_tile * BM;
   const uint32_t n0 = a.n_base + n_tile * BN;
 
   if constexpr (SD) {
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? ((BM / MT) * 
     if (a.vec_out && nq + 3 < a.n_gemm) {
       uint32_t img, rem;
       a.fd_hw.divmod(nq, img, rem);
-      float* base = a.out + static_cast<int64_t>(img) * a.M * a.hw + rem;
+      float* base = a.out + static_cast<int64_t>(img) * a.co_out * a.hw + rem;
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
         const int m = m0 + (i / 4) * (BM / 2) + ty * 4 + (i % 4);
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__((BM / MT) * (BN / MT), MT == 8 ? ((BM / MT) * 
         if (n >= a.n_gemm) continue;
         uint32_t img, rem;
         a.fd_hw.divmod(n, img, rem);
-        float* base = a.out + static_cast<int64_t>(img) * a.M * a.hw + rem;
+        float* base = a.out + static_cast<int64_t>(img) * a.co_out * a.hw + rem;
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
           const int m = m0 + (i / 4) * (BM / 2) + ty * 4 + (i % 4);
@@ -514,7 +516,7 @@ __global__ void __launch_bounds__(256, 2) conv_simt_smallk_kernel(const ConvArgs
       if (a.vec_out && nq + 3 < a.n_gemm) {
         uint32_t img, rem;
         a.fd_hw.divmod(nq, img, rem);
-        float* base = a.out + static_cast<int64_t>(img) * a.M * a.hw + rem;
+        float* base = a.out + static_cast<int64_t>(img) * a.co_out * a.hw + rem;
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
           const int m = (i / 4) * (BM / 2) + ty * 4 + (i % 4);
@@ -529,7 +531,7 @@ __global__ void __launch_bounds__(256, 2) conv_simt_smallk_kernel(const ConvArgs
           if (n >= a.n_gemm) continue;
           uint32_t img, rem;
           a.fd_hw.divmod(n, img, rem);
-          float* base = a.out + static_cast<int64_t>(img) * a.M * a.hw + rem;
+          float* base = a.out + static_cast<int64_t>(img) * a.co_out * a.hw + rem;
 #pragma unroll
           for (int i = 0; i < MT; ++i) {
             const int m = (i / 4) * (BM / 2) + ty * 4 + (i % 4);
@@ -576,7 +578,7 @@ constexpr int kDeltaSmemMax = IM2WIN_SIMT_SDELTA ? 48 * 1024 : 0;  // bytes of d
 template <int BM, int BN, int BK, int STAGES, bool EXACT, bool VEC, int MT>
 static cudaError_t launch_cfg(const ConvArgs& a0, cudaStream_t stream) {
   ConvArgs a = a0;
-  a.m_tiles = (a.M + BM - 1) / BM;
+  a.m_tiles = (a.M - a.m_base + BM - 1) / BM;
   uint64_t n_tiles = (static_cast<uint64_t>(a.n_gemm - a.n_base) + BN - 1) / BN;
   uint64_t grid = n_tiles * a.m_tiles;
   const bool sd = static_cast<size_t>(a.Kp) * 4 <= kDeltaSmemMax;
@@ -680,6 +682,7 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
   a.delta = delta;
   a.out = out;
   a.M = static_cast<int>(c_out);
+  a.co_out = static_cast<uint32_t>(c_out);
   a.Mp = Mp;
   a.K = static_cast<int>(K);
   a.Kp = Kp;
@@ -761,7 +764,21 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
         tail_cfg = 4;
       }
     }
-    if (tail_cfg >= 0 && n_main > 0 && n_main < static_cast<uint32_t>(n_gemm)) {
+    // 96-channel layers (library choice): channels 0-63 on the 64x256 tile, 64-95 on 32x128
+    // 4x4-micro-tile CTAs -- both issue the packed exact pairs, which the 96x128 tile does not
+    // profit from (IM2WIN_SIMT_SPLIT96=0 keeps the single 96x128 launch).  Same bits.
+    const char* s96 = getenv("IM2WIN_SIMT_SPLIT96");
+    if (auto_cfg && vec && stages > 1 && cfg == 2 && c_out == 96 && IM2WIN_SIMT_FP2 && !(s96 && atoi(s96) == 0)) {
+      ConvArgs a64 = a;
+      a64.M = 64;
+      e = dispatch(1, a64);
+      if (e == cudaSuccess) {
+        ConvArgs a32 = a;
+        a32.m_base = 64;
+        e = dispatch(6, a32);
+        im2win_label_kernel("conv_simt_kernel (channels 0-63 on 64x256 8x8 tiles, 64-95 on 32x128 4x4 tiles)");
+      }
+    } else if (tail_cfg >= 0 && n_main > 0 && n_main < static_cast<uint32_t>(n_gemm)) {
       ConvArgs am = a;
       am.n_gemm = n_main;
       e = dispatch(cfg, am);
@@ -867,7 +884,7 @@ __global__ void __launch_bounds__(256) conv_simt_1x1_kernel(const ConvArgs a) {
   if (m < a.M && n < a.n_gemm) {
     uint32_t img, rem;
     a.fd_hw.divmod(n, img, rem);
-    a.out[static_cast<int64_t>(img) * a.M * a.hw + static_cast<int64_t>(m) * a.hw + rem] = acc;
+    a.out[static_cast<int64_t>(img) * a.co_out * a.hw + static_cast<int64_t>(m) * a.hw + rem] = acc;
   }
 }
 
@@ -897,7 +914,8 @@ int im2win_launch_conv_simt_1x1(const float* win, const float* flt, float* out, 
   a.img_stride = static_cast<uint32_t>(c_in * h_out * row_len);
   a.row_stride = static_cast<uint32_t>(row_len);
   a.col_stride = static_cast<uint32_t>(stride * h_f);
-  a.M = static_cast<int>(c_out); a.Mp = Mp; a.K = static_cast<int>(K); a.Kp = Kp;
+  a.M = static_cast<int>(c_out); a.co_out = static_cast<uint32_t>(c_out); a.Mp = Mp; a.K = static_cast<int>(K);
+  a.Kp = Kp;
   a.n_gemm = static_cast<uint32_t>(n_gemm);
   a.c_in = static_cast<uint32_t>(c_in); a.h_out = static_cast<uint32_t>(h_out);
   a.w_out = static_cast<uint32_t>(w_out); a.row_len = static_cast<uint32_t>(row_len);
