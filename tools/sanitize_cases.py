@@ -65,6 +65,11 @@ for (n, c, h, w, co, hf, wf, s) in [(2, 64, 17, 19, 64, 7, 7, 2), (3, 32, 9, 10,
             assert "tap pairs" in pkg._lib.last_kernel(), pkg._lib.last_kernel()
         for k in env:
             del os.environ[k]
+# a 96-channel layer big enough for the library's 64 + 32 channel split (packed exact MACs)
+x = torch.from_numpy(rng.standard_normal((32, 3, 131, 131), dtype=np.float32)).cuda()
+f = torch.from_numpy(rng.standard_normal((96, 3, 11, 11), dtype=np.float32)).cuda()
+pkg.conv_im2win_opt(x, f, pkg.ConvParams(3, 96, 11, 11, 4))
+assert "64-95" in pkg._lib.last_kernel(), pkg._lib.last_kernel()
 # 4-byte-offset operands (the staged transform aligns its 16-byte copies to the address)
 for (n, c, h, w, co, hf, wf, s, p) in cases[:3]:
     base = torch.from_numpy(rng.standard_normal(1 + n * c * h * w, dtype=np.float32)).cuda()
