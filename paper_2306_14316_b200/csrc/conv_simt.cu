@@ -628,7 +628,10 @@ extern "C" int im2win_simt_pick(int M, long long n_gemm, int K) {
 static const int kNumCfg = 7;
 static const int kBM[kNumCfg] = {128, 64, 96, 128, 64, 128, 32};
 // CTA tile N extents, for reference: {128, 256, 128, 64, 64, 32, 128}
-static const int kBKc[kNumCfg] = {16, 16, 16, 16, 16, 16, 16};
+// The 64x256 tile's production kernel runs 32-deep K-slabs in 2 stages (half the slab barriers
+// and loop overhead; with the packed exact pairs its body fits the instruction cache): conv4/conv8
+// +0.6%, conv9 +1.3%, conv11 +2% over 16-deep slabs in 3 stages (scalar FMUL+FADD: 23 vs 30 TF).
+static const int kBKc[kNumCfg] = {16, 32, 16, 16, 16, 16, 16};
 static const int kMaxBK = 32;
 
 // nchw_hw == nullptr: `win` is the im2win tensor Ĩ (row_len = Hf * w_eff).  Otherwise `win` is the
@@ -656,7 +659,13 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
     return 1;
   }
   if (cfg >= 4 && !(vec && stages > 1)) cfg = static_cast<int>(c_out) <= 64 ? 1 : 0;  // ablations: 8x8 tiles
-  const int BM = kBM[cfg], BK = kBKc[cfg];
+  // 96-channel layers (library choice): channels 0-63 on the 64x256 tile, 64-95 on 32x128 4x4-
+  // micro-tile CTAs -- both issue the packed exact pairs, which the 96x128 tile does not profit
+  // from (IM2WIN_SIMT_SPLIT96=0 keeps the single 96x128 launch).  Same bits.
+  const char* s96 = getenv("IM2WIN_SIMT_SPLIT96");
+  const bool split96 = auto_cfg && vec && stages > 1 && cfg == 2 && c_out == 96 && IM2WIN_SIMT_FP2 &&
+                       !(s96 && atoi(s96) == 0);
+  const int BM = kBM[cfg], BK = split96 ? kBKc[1] : kBKc[cfg];  // K padded for every launch's slab
   const int Mp = static_cast<int>((c_out + BM - 1) / BM * BM);
   const int Kp = static_cast<int>((K + BK - 1) / BK * BK);
   if ((reinterpret_cast<uintptr_t>(workspace) & 15u) != 0) {
@@ -729,7 +738,11 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
       cudaError_t e = cudaSuccess;
       switch (c) {
         case 0: { IM2WIN_DISPATCH(128, 128, 16) break; }
-        case 1: { IM2WIN_DISPATCH(64, 256, 16) break; }
+        case 1: {
+          if (exact && vec && stages == 3 && IM2WIN_SIMT_FP2) e = launch_cfg<64, 256, 32, 2, true, true, 8>(a, stream);
+          else { IM2WIN_DISPATCH(64, 256, 16) }
+          break;
+        }
         case 2: { IM2WIN_DISPATCH(96, 128, 16) break; }
         case 3: { IM2WIN_DISPATCH(128, 64, 16) break; }
         case 4: { IM2WIN_DISPATCH4(64, 64, 16) break; }
@@ -764,11 +777,7 @@ int im2win_launch_conv_simt(const float* win, const float* flt, float* out, void
         tail_cfg = 4;
       }
     }
-    // 96-channel layers (library choice): channels 0-63 on the 64x256 tile, 64-95 on 32x128
-    // 4x4-micro-tile CTAs -- both issue the packed exact pairs, which the 96x128 tile does not
-    // profit from (IM2WIN_SIMT_SPLIT96=0 keeps the single 96x128 launch).  Same bits.
-    const char* s96 = getenv("IM2WIN_SIMT_SPLIT96");
-    if (auto_cfg && vec && stages > 1 && cfg == 2 && c_out == 96 && IM2WIN_SIMT_FP2 && !(s96 && atoi(s96) == 0)) {
+    if (split96) {
       ConvArgs a64 = a;
       a64.M = 64;
       e = dispatch(1, a64);
