@@ -141,6 +141,18 @@ IM2WIN_DEVICE void mac_row(float (&acc)[MT], float a, const float (&fb)[MT], flo
     }
     return;
   }
+  if constexpr (!EXACT && FP2) {
+    // the FFMA variant: one packed FFMA2 per pair (per component the same as __fmaf_rn)
+#pragma unroll
+    for (int j = 0; j < MT; j += 2) {
+      uint64_t c;
+      asm("{\n\t.reg .b64 aa, bb, cc;\n\tmov.b64 aa, {%1, %1};\n\tmov.b64 bb, {%2, %3};\n\t"
+          "mov.b64 cc, {%4, %5};\n\tfma.rn.f32x2 %0, aa, bb, cc;\n\t}\n"
+          : "=l"(c) : "f"(a), "f"(fb[j]), "f"(fb[j + 1]), "f"(acc[j]), "f"(acc[j + 1]));
+      asm("mov.b64 {%0, %1}, %2;\n" : "=f"(acc[j]), "=f"(acc[j + 1]) : "l"(c));
+    }
+    return;
+  }
 #endif
   (void)nz;
   (void)one;
